@@ -1,0 +1,124 @@
+"""Hand-built edge-case inputs (packed layouts), mirroring what the
+reference's own tests exercise:
+
+- the 12-record golden corpus (tests/data/golden_input.jsonl, 9 3x3 + 3 2x2);
+- scalar matrices (test_acceptance.py:118-121), diag(3,2,1) and its
+  permutations (test_eig3_angles.py:29, 183-200);
+- separated double roots and near-boundary gaps 1e-3/1e-6/1e-9 built from QR
+  factors (test_acceptance.py:105-132, test_eig3_angles.py:165-218);
+- conjugation round trips with solver-order eigenvalues (conftest.py:42-50);
+- zero f-vector patterns, signed zeros, tiny / subnormal / huge magnitudes
+  (overflow in `**`), NaN / inf entries.
+All generated deterministically from fixed seeds; no reference code needed.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+_UP = ((0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2))
+
+
+def _pack(m):
+    m = np.asarray(m, dtype=float)
+    s = 0.5 * (m + m.T)
+    return [m[0, 0], s[0, 1], s[0, 2], m[1, 1], s[1, 2], m[2, 2]]
+
+
+def _rot(p1, p2, p3):
+    c1, s1 = math.cos(p1), math.sin(p1)
+    c2, s2 = math.cos(p2), math.sin(p2)
+    c3, s3 = math.cos(p3), math.sin(p3)
+    rx = np.array([[1, 0, 0], [0, c1, -s1], [0, s1, c1]])
+    ry = np.array([[c2, 0, s2], [0, 1, 0], [-s2, 0, c2]])
+    rz = np.array([[c3, -s3, 0], [s3, c3, 0], [0, 0, 1]])
+    return rx @ ry @ rz
+
+
+def _conj(phis, lams):
+    d = _rot(*phis)
+    return _pack((d * np.asarray(lams, dtype=float)) @ d.T)
+
+
+def edge_cases_3x3() -> np.ndarray:
+    rows = []
+    # golden corpus 3x3 records, packed (a11,a12,a13,a22,a23,a33)
+    rows += [
+        [1, 0, 0, 1, 0, 1],
+        [2.5, 0, 0, 2.5, 0, 2.5],
+        [3, 0, 0, 2, 0, 1],
+        [0, 1, 1, 0, 1, 0],
+        [1.6811788772383369, 0, -0.4660195429836132, 2, 0, 1.3188211227616633],
+        [5, 0, 0, 1, -2.1285471334023225e-17, 1],
+        [1.8250200448230833, 0.78821148340683078, 0.34388344776385738,
+         2.4664238340913922, -0.3064514246013107, 1.7085561210855242],
+        [0.25, 0.125, -0.375, -0.5, 0.625, 0.75],
+        [3, 1e-08, 0, 2, -1e-08, 1],
+    ]
+    for c in (-7.0, -1.0, 0.0, 0.25, 1.0, 3.5):
+        rows.append([c, 0, 0, c, 0, c])
+    for d in ((3, 2, 1), (1, 2, 3), (2, 3, 1), (2, 1, 3), (3, 1, 2), (1, 3, 2),
+              (2, 2, 1), (1, 2, 2), (2, 1, 2), (5, 1, 1), (1, 1, 5), (-1, 0, 1)):
+        rows.append([d[0], 0, 0, d[1], 0, d[2]])
+    # one nonzero off-diagonal entry (f1 = 0 or f2 = 0 patterns)
+    rows += [[1, 0.5, 0, 2, 0, 3], [1, 0, 0.5, 2, 0, 3], [1, 0, 0, 2, 0.5, 3],
+             [2, 0, 0, 2, 0.5, 2], [1, 0.3, 0, 1, 0, 4], [0, 0, 1, 0, 0, 0],
+             [1, 0, 0, 1, 0, 2], [1, 0, 0, 3, 0, 3], [0, 1, 0, 0, 0, 0],
+             [1, 0, 0, 2, 0, 2], [2, 0, 0, 1, 1e-20, 1]]
+    # signed zeros
+    rows += [[-0.0, -0.0, -0.0, -0.0, -0.0, -0.0], [1, -0.0, 0.0, 2, -0.0, 3],
+             [0.0, 1.0, -0.0, 0.0, -0.0, 0.0]]
+    # conjugated round trips at the constructing (largest, smallest, middle)
+    rng = np.random.default_rng(7001)
+    for _ in range(60):
+        phis = rng.uniform(-math.pi / 2 + 0.05, math.pi / 2 - 0.05, 3)
+        lams = np.sort(rng.uniform(-4.0, 4.0, 3))
+        rows.append(_conj(phis, (lams[2], lams[0], lams[1])))
+    # angles at / near 0, pi/4, pi/2 (refinement windows)
+    for p in (0.0, 1e-9, 1e-5, 0.1, math.pi / 8, math.pi / 4, 3 * math.pi / 8,
+              math.pi / 2 - 1e-5, math.pi / 2):
+        rows.append(_conj((0.3, p, 0.7), (3.0, 1.0, 2.0)))
+        rows.append(_conj((0.3, 0.7, p), (3.0, 1.0, 2.0)))
+        rows.append(_conj((p, 0.4, 0.9), (3.0, 1.0, 2.0)))
+    # separated double roots (test_acceptance.py:105-117 construction)
+    rng = np.random.default_rng(7002)
+    for _ in range(40):
+        lam = rng.uniform(-3.0, 3.0)
+        lam3 = lam + math.copysign(rng.uniform(0.5, 3.0), rng.uniform(-1, 1))
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        rows.append(_pack((q * np.array([lam, lam, lam3])) @ q.T))
+    # near-boundary gaps (test_acceptance.py:124-131)
+    for gap in (1e-3, 1e-6, 1e-9, 1e-12):
+        for _ in range(15):
+            lam = rng.uniform(-3.0, 3.0)
+            q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+            rows.append(_pack((q * np.array([lam, lam + gap, lam + 2.0])) @ q.T))
+    # conjugated double roots about single axes (test_eig3_angles.py:150-170)
+    rows.append(_conj((0.0, 0.6, 0.0), (2.0, 2.0, 1.0)))
+    rows.append(_conj((0.4, 0.0, 0.0), (5.0, 1.0, 1.0)))
+    # magnitudes: tiny, subnormal, large, overflowing `**`
+    base = np.array([0.25, 0.125, -0.375, -0.5, 0.625, 0.75])
+    for s in (1e-300, 1e-200, 1e-160, 1e-100, 1e-20, 1e20, 1e40, 1e50, 1e52,
+              1e60, 1e100, 1e155, 1e200):
+        rows.append(list(base * s))
+    rows.append([5e-324, 0, 0, 1e-323, 0, 0])
+    # non-finite inputs
+    rows += [[math.nan, 0, 0, 1, 0, 1], [1, math.inf, 0, 1, 0, 1],
+             [1, 0, 0, 1, 0, -math.inf]]
+    return np.array(rows, dtype=np.float64)
+
+
+def edge_cases_2x2() -> np.ndarray:
+    rows = [[1, 0, 1], [2, 1, 2], [1, 2, 0], [3, 0, 1], [1, 0, 3], [0, 0, 0],
+            [-0.0, -0.0, -0.0], [0, 1, 0], [0, -1, 0], [1, 1e-15, 1],
+            [1, 1e-13, 1], [1 + 1e-15, 0, 1], [2, -1, 2], [-1, 0, 1],
+            [1e-300, 1e-300, 0], [1e200, 1e200, -1e200], [1e160, 1, 0],
+            [5e-324, 5e-324, 0], [math.nan, 0, 1], [1, math.inf, 1]]
+    rng = np.random.default_rng(7003)
+    for _ in range(40):
+        a11, a12, a22 = rng.uniform(-1, 1, 3)
+        rows.append([a11, a12, a22])
+        rows.append([a22, a12, a11])       # swap symmetry pair
+    return np.array(rows, dtype=np.float64)

@@ -1,0 +1,74 @@
+"""Freeze golden fixtures from the UNMODIFIED reference implementation.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports `symdiag` in place from /root/reference/pkg/src (read-only,
+PYTHONDONTWRITEBYTECODE), runs diagonalize3 / diagonalize2 and the stage
+functions row by row over seeded inputs, and writes compressed .npz files
+next to this script.  The GPU box never needs the reference: the tests read
+only these files.
+
+Sets (prefixes of the benchmark configs are exact, see workloads.py):
+  eig3_edge  hand-built edge cases (cases.py)
+  eig3_c2    first 2048 rows of config 2 (N(0,1), seed 1)
+  eig3_c3    first 4096 rows of config 3 (degenerate stress, seed 2)
+  eig3_c4    first 2048 rows of config 4 (SPD fp32, seed 3; upcast exactly)
+  eig3_u11   2048 U[-1,1] rows, seed 101 (acceptance criterion 1 style)
+  eig2_c1    2x2 edge cases + first 4096 rows of config 1 (seed 0)
+  stages_*   char_coeffs / compute_pq / eigenvalues3 / pq_expanded /
+             compute_v / compute_w on the edge + c3 sets
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE))
+sys.path.insert(0, str(HERE.parents[1]))
+
+import cases  # noqa: E402
+import refrun  # noqa: E402
+from paper_1306_6291_b200 import workloads  # noqa: E402
+
+
+def save(name, **arrays):
+    np.savez_compressed(HERE / f"{name}.npz", **arrays)
+    print(f"wrote {name}.npz", {k: v.shape for k, v in arrays.items()})
+
+
+def main():
+    if not refrun.available():
+        raise SystemExit("reference not available at " + refrun.REF_SRC)
+    sets3 = {
+        "edge": cases.edge_cases_3x3(),
+        "c2": workloads.generate("c2", 2048),
+        "c3": workloads.generate("c3", 4096),
+        "c4": workloads.generate("c4", 2048),
+        "u11": np.random.default_rng(101).uniform(-1.0, 1.0, (2048, 6)),
+    }
+    for name, A in sets3.items():
+        A32 = A if A.dtype == np.float32 else None
+        A64 = np.asarray(A, dtype=np.float64)
+        r = refrun.run_eig3(A64, with_d=(name == "edge"))
+        extra = dict(A32=A32) if A32 is not None else {}
+        if name == "edge":
+            extra["d"] = r["d"]
+        save(f"eig3_{name}", A=A64, lam=r["lam"], ang=r["ang"],
+             status=r["status"], report=r["report"], **extra)
+    A2 = np.concatenate([cases.edge_cases_2x2(), workloads.generate("c1", 4096)])
+    r = refrun.run_eig2(A2, with_d=True)
+    save("eig2_c1", A=A2, lam=r["lam"], phi=r["phi"], status=r["status"], d=r["d"])
+    for name in ("edge", "c3"):
+        A = sets3[name]
+        s = refrun.run_stages(A)
+        save(f"stages_{name}", A=A, **s)
+
+
+if __name__ == "__main__":
+    main()
