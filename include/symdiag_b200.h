@@ -125,10 +125,13 @@ int sd_eigenvalues3_f64(const double* bcd, const double* pqd, int64_t n,
 /* pq_expanded (eig3.py:112-126): pq[n][2]; status as sd_char_coeffs_f64. */
 int sd_pq_expanded_f64(const double* A, int64_t n, double* pq,
                        uint8_t* status, void* cuda_stream);
-/* compute_v (eig3.py:183-195) and compute_w (eig3.py:198-206): vw[n][2];
- * status: 0, SD_STAGE_DEGENERATE_EIGENVALUES or SD_ERR_DOMAIN_EXCURSION.   */
-int sd_compute_vw_f64(const double* A, const double* lam, int64_t n,
-                      double* vw, uint8_t* status, void* cuda_stream);
+/* compute_v (eig3.py:183-195): v[n]; status: 0,
+ * SD_STAGE_DEGENERATE_EIGENVALUES or SD_ERR_DOMAIN_EXCURSION.              */
+int sd_compute_v_f64(const double* A, const double* lam, int64_t n,
+                     double* v, uint8_t* status, void* cuda_stream);
+/* compute_w (eig3.py:198-206) for caller-given v[n]: w[n]; status as above. */
+int sd_compute_w_f64(const double* A, const double* lam, const double* v,
+                     int64_t n, double* w, uint8_t* status, void* cuda_stream);
 /* resolve_signs (eig3.py:269-386) for given lambdas and v, w.  ang[n][3],
  * status carries the sign / near-tie flags; report (nullable) as above.
  * BothFVectorsZero is reported as SD_STAGE_BOTH_F_ZERO.                    */
@@ -163,6 +166,13 @@ int sd_eig3_f32_host(sd_plan* plan, const float* A, int64_t n, float* lam,
                      float* ang, uint8_t* status);
 int sd_eig2_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
                      double* phi, uint8_t* status);
+
+/* ---- diagnostics --------------------------------------------------------- */
+/* FP64-pipe peak probe for the roofline denominator: `blocks` x 256 threads,
+ * each runs `iters` x 16 independent DFMA chains; *dfma_total receives the
+ * DFMA count (time it with events on `cuda_stream`).  sink[blocks*256].     */
+int sd_probe_dfma(int blocks, int iters, double* sink, double* dfma_total,
+                  void* cuda_stream);
 
 /* ---- misc --------------------------------------------------------------- */
 const char* sd_last_error(void);   /* thread-local message of the last error */

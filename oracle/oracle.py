@@ -47,6 +47,7 @@ def lib():
         L.sdo_eigenvalues3.argtypes = [P, P, I64, P]
         L.sdo_pq_expanded.argtypes = [P, I64, P, P]
         L.sdo_compute_vw.argtypes = [P, P, I64, P, P]
+        L.sdo_compute_w.argtypes = [P, P, P, I64, P, P]
         L.sdo_resolve_signs.argtypes = [P, P, P, I64, P, P, P]
         L.sdo_degenerate_double.argtypes = [P, P, I64, P, P, P]
         L.sdo_g_vectors.argtypes = [P, I64, P]
@@ -139,6 +140,15 @@ def compute_vw(A, lam):
     n = A.shape[0]
     out, st = np.empty((n, 2)), np.empty(n, np.uint8)
     lib().sdo_compute_vw(_p(A), _p(lam), n, _p(out), _p(st))
+    return out, st
+
+
+def compute_w(A, lam, v):
+    A, lam = _c(A, width=6), _c(lam, width=3)
+    v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
+    n = A.shape[0]
+    out, st = np.empty(n), np.empty(n, np.uint8)
+    lib().sdo_compute_w(_p(A), _p(lam), _p(v), n, _p(out), _p(st))
     return out, st
 
 

@@ -1,0 +1,285 @@
+"""Batched tensor API: the B200 hot path.
+
+Every function takes CUDA tensors in the packed layouts of
+include/symdiag_b200.h and launches one kernel of libsymdiag_b200.so on the
+current torch stream.  Outputs are freshly allocated (or caller-provided via
+`out=`) CUDA tensors; per-matrix outcomes are in the uint8 `status` tensor
+(see status.py), never raised.
+
+Reference functions replaced (/root/reference/pkg/src/symdiag):
+  diagonalize3_batched  <- diagonalize3 + euler_angles   eig3.py:509-576
+  diagonalize2_batched  <- diagonalize2                  eig2.py:44-48
+  char_coeffs_batched   <- char_coeffs                   eig3.py:102-109
+  compute_pq_batched    <- compute_pq                    eig3.py:129-156
+  eigenvalues3_batched  <- eigenvalues3                  eig3.py:159-174
+  pq_expanded_batched   <- pq_expanded                   eig3.py:112-126
+  compute_v_batched / compute_w_batched <- compute_v/w   eig3.py:183-206
+  resolve_signs_batched <- resolve_signs                 eig3.py:269-386
+  degenerate_double_batched <- degenerate_double         eig3.py:389-454
+  f_vectors_batched / g_vectors_batched                  eig3.py:209-225
+  compose_rotation_batched <- compose_rotation           core.py:229-235
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple, Optional
+
+import torch
+
+from . import _lib
+
+REPORT_STRIDE = _lib.REPORT_STRIDE
+
+
+class Eig3Batch(NamedTuple):
+    lam: torch.Tensor        # [n,3] solver order
+    ang: torch.Tensor        # [n,3] (phi1, phi2, phi3) = Euler angles
+    status: torch.Tensor     # [n] uint8
+    report: Optional[torch.Tensor] = None  # [n,24] fp64 SolveReport rows
+    d: Optional[torch.Tensor] = None       # [n,9] fp64 eigenvector matrix
+
+    @property
+    def euler(self) -> torch.Tensor:
+        """euler_angles (eig3.py:568-576): the same triple, no extra storage."""
+        return self.ang
+
+
+class Eig2Batch(NamedTuple):
+    lam: torch.Tensor        # [n,2]
+    phi: torch.Tensor        # [n]
+    status: torch.Tensor     # [n] uint8
+    d: Optional[torch.Tensor] = None       # [n,4] fp64 rot2(phi)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check_input(A: torch.Tensor, width: int, dtypes=(torch.float64,)) -> torch.Tensor:
+    if not isinstance(A, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if not A.is_cuda:
+        _lib.require_cuda()
+        raise _lib.CudaUnavailable("input must be a CUDA tensor (no CPU path)")
+    if A.dtype not in dtypes:
+        raise TypeError(f"dtype {A.dtype} not in {dtypes}")
+    if A.dim() == 1:
+        A = A.view(-1, width)
+    if A.dim() != 2 or A.shape[1] != width:
+        raise ValueError(f"expected shape [n, {width}], got {tuple(A.shape)}")
+    return A.contiguous()
+
+
+def _alloc(out, key, shape, dtype, device):
+    if out is not None and key in out and out[key] is not None:
+        t = out[key]
+        if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous():
+            raise ValueError(f"out[{key!r}] must be contiguous {dtype} {tuple(shape)}")
+        return t
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
+def diagonalize3_batched(A: torch.Tensor, *, report: bool = False, with_d: bool = False,
+                         out: Optional[dict] = None, stream=None) -> Eig3Batch:
+    """Batched diagonalize3 over packed A[n,6] (fp64, or fp32 with fp64
+    internals).  `report`/`with_d` (fp64 only) add SolveReport rows and D."""
+    A = _check_input(A, 6, (torch.float64, torch.float32))
+    n, dev, dt = A.shape[0], A.device, A.dtype
+    with torch.cuda.device(dev):
+        lam = _alloc(out, "lam", (n, 3), dt, dev)
+        ang = _alloc(out, "ang", (n, 3), dt, dev)
+        st = _alloc(out, "status", (n,), torch.uint8, dev)
+        rep = d = None
+        if report or with_d:
+            if dt != torch.float64:
+                raise TypeError("report/with_d need fp64 input")
+            rep = _alloc(out, "report", (n, REPORT_STRIDE), torch.float64, dev) if report else None
+            d = _alloc(out, "d", (n, 9), torch.float64, dev) if with_d else None
+            _lib.call("sd_eig3_report_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
+                      st.data_ptr(), _ptr(rep), _ptr(d), _stream(stream))
+        elif dt == torch.float64:
+            _lib.call("sd_eig3_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
+                      st.data_ptr(), _stream(stream))
+        else:
+            _lib.call("sd_eig3_f32", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
+                      st.data_ptr(), _stream(stream))
+    return Eig3Batch(lam, ang, st, rep, d)
+
+
+def diagonalize2_batched(A: torch.Tensor, *, with_d: bool = False,
+                         out: Optional[dict] = None, stream=None) -> Eig2Batch:
+    """Batched diagonalize2 over packed A[n,3] = (a11, a12, a22)."""
+    A = _check_input(A, 3)
+    n, dev = A.shape[0], A.device
+    with torch.cuda.device(dev):
+        lam = _alloc(out, "lam", (n, 2), torch.float64, dev)
+        phi = _alloc(out, "phi", (n,), torch.float64, dev)
+        st = _alloc(out, "status", (n,), torch.uint8, dev)
+        d = None
+        if with_d:
+            d = _alloc(out, "d", (n, 4), torch.float64, dev)
+            _lib.call("sd_eig2_report_f64", A.data_ptr(), n, lam.data_ptr(), phi.data_ptr(),
+                      st.data_ptr(), d.data_ptr(), _stream(stream))
+        else:
+            _lib.call("sd_eig2_f64", A.data_ptr(), n, lam.data_ptr(), phi.data_ptr(),
+                      st.data_ptr(), _stream(stream))
+    return Eig2Batch(lam, phi, st, d)
+
+
+def _empty(n, w, dev, dtype=torch.float64):
+    return torch.empty((n, w) if w else (n,), dtype=dtype, device=dev)
+
+
+def char_coeffs_batched(A):
+    A = _check_input(A, 6)
+    n, dev = A.shape[0], A.device
+    bcd, st = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_char_coeffs_f64", A.data_ptr(), n, bcd.data_ptr(), st.data_ptr(), _stream())
+    return bcd, st
+
+
+def compute_pq_batched(bcd):
+    bcd = _check_input(bcd, 3)
+    n, dev = bcd.shape[0], bcd.device
+    pqd, st = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_compute_pq_f64", bcd.data_ptr(), n, pqd.data_ptr(), st.data_ptr(), _stream())
+    return pqd, st
+
+
+def eigenvalues3_batched(bcd, pqd):
+    bcd, pqd = _check_input(bcd, 3), _check_input(pqd, 3)
+    n, dev = bcd.shape[0], bcd.device
+    lam = _empty(n, 3, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_eigenvalues3_f64", bcd.data_ptr(), pqd.data_ptr(), n, lam.data_ptr(),
+                  _stream())
+    return lam
+
+
+def pq_expanded_batched(A):
+    A = _check_input(A, 6)
+    n, dev = A.shape[0], A.device
+    pq, st = _empty(n, 2, dev), _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_pq_expanded_f64", A.data_ptr(), n, pq.data_ptr(), st.data_ptr(), _stream())
+    return pq, st
+
+
+def compute_v_batched(A, lam):
+    A, lam = _check_input(A, 6), _check_input(lam, 3)
+    n, dev = A.shape[0], A.device
+    v, st = _empty(n, 0, dev), _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_compute_v_f64", A.data_ptr(), lam.data_ptr(), n, v.data_ptr(),
+                  st.data_ptr(), _stream())
+    return v, st
+
+
+def compute_w_batched(A, lam, v):
+    A, lam = _check_input(A, 6), _check_input(lam, 3)
+    v = _check_input(v.reshape(-1, 1), 1)
+    n, dev = A.shape[0], A.device
+    w, st = _empty(n, 0, dev), _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_compute_w_f64", A.data_ptr(), lam.data_ptr(), v.data_ptr(), n,
+                  w.data_ptr(), st.data_ptr(), _stream())
+    return w, st
+
+
+def resolve_signs_batched(A, lam, vw):
+    A, lam, vw = _check_input(A, 6), _check_input(lam, 3), _check_input(vw, 2)
+    n, dev = A.shape[0], A.device
+    ang, st, rep = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8), _empty(n, REPORT_STRIDE, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_resolve_signs_f64", A.data_ptr(), lam.data_ptr(), vw.data_ptr(), n,
+                  ang.data_ptr(), st.data_ptr(), rep.data_ptr(), _stream())
+    return ang, st, rep
+
+
+def degenerate_double_batched(A, lam2):
+    A, lam2 = _check_input(A, 6), _check_input(lam2, 2)
+    n, dev = A.shape[0], A.device
+    ang, st, rep = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8), _empty(n, REPORT_STRIDE, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_degenerate_double_f64", A.data_ptr(), lam2.data_ptr(), n, ang.data_ptr(),
+                  st.data_ptr(), rep.data_ptr(), _stream())
+    return ang, st, rep
+
+
+def f_vectors_batched(A):
+    A = _check_input(A, 6)
+    n, dev = A.shape[0], A.device
+    f = _empty(n, 4, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_f_vectors_f64", A.data_ptr(), n, f.data_ptr(), _stream())
+    return f
+
+
+def g_vectors_batched(inp):
+    """inp[n,7] = (l1, l2, l3, phi2, phi3, v, w) -> g[n,4] = (g1x, g1y, g2x, g2y)."""
+    inp = _check_input(inp, 7)
+    n, dev = inp.shape[0], inp.device
+    g = _empty(n, 4, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_g_vectors_f64", inp.data_ptr(), n, g.data_ptr(), _stream())
+    return g
+
+
+def compose_rotation_batched(ang):
+    ang = _check_input(ang, 3)
+    n, dev = ang.shape[0], ang.device
+    d = _empty(n, 9, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_compose_rotation_f64", ang.data_ptr(), n, d.data_ptr(), _stream())
+    return d
+
+
+class HostPlan:
+    """End-to-end path over HOST buffers (numpy or pinned torch CPU tensors):
+    chunked H2D -> kernel -> D2H, pipelined over three streams in C++
+    (sd_host.cu).  Use pinned memory for full copy/compute overlap."""
+
+    def __init__(self, device: int = 0, chunk: int = 1 << 22):
+        import ctypes
+        _lib.require_cuda()
+        self._h = ctypes.c_void_p()
+        _lib.call("sd_plan_create", device, chunk, ctypes.byref(self._h))
+        self.device, self.chunk = device, chunk
+
+    def close(self):
+        if self._h:
+            _lib.load().sd_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 — interpreter shutdown
+            pass
+
+    @staticmethod
+    def _hp(x):
+        if isinstance(x, torch.Tensor):
+            if x.is_cuda or not x.is_contiguous():
+                raise ValueError("host buffers must be contiguous CPU tensors")
+            return x.data_ptr()
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("host buffers must be C-contiguous")
+        return x.ctypes.data
+
+    def eig3(self, A, lam, ang, status):
+        n = A.shape[0]
+        name = "sd_eig3_f32_host" if A.dtype in (torch.float32,) or str(A.dtype) == "float32" \
+            else "sd_eig3_f64_host"
+        _lib.call(name, self._h, self._hp(A), n, self._hp(lam), self._hp(ang), self._hp(status))
+
+    def eig2(self, A, lam, phi, status):
+        _lib.call("sd_eig2_f64_host", self._h, self._hp(A), A.shape[0], self._hp(lam),
+                  self._hp(phi), self._hp(status))

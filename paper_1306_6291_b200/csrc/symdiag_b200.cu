@@ -1,0 +1,490 @@
+// symdiag_b200.cu — kernels and the C ABI (include/symdiag_b200.h).
+//
+// Hot path: one thread per matrix, fp64 in registers.  Each warp stages its
+// 32 packed input rows through shared memory with 8/16-byte vector loads so
+// global reads are fully coalesced (48 B x 32 = 1536 B contiguous per warp),
+// then every lane runs the closed form on its own row.  There is no
+// block-wide barrier: warps of a block never wait for one another, so the
+// long, branchy fp64 body of one warp overlaps the others' memory phases.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false
+//        -lineinfo (see __graft_entry__.build()).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/symdiag_b200.h"
+#include "sd_eig2.cuh"
+#include "sd_eig3.cuh"
+
+namespace {
+
+constexpr int kWarps = 4;  // warps per block
+constexpr int kThreads = 32 * kWarps;
+
+thread_local char g_err[512] = "";
+thread_local int64_t g_launches = 0;
+
+int set_err(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t st = cudaGetLastError();
+  if (st != cudaSuccess) {
+    char buf[400];
+    snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(st));
+    return set_err(SD_ECUDA, buf);
+  }
+  g_launches++;
+  return SD_OK;
+}
+
+inline unsigned grid_for(int64_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
+
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+
+// Stage W values per row of this warp's 32 rows into shared memory.
+// `vec` selects 2-wide vector loads (the base pointer is 2*sizeof(T)-aligned
+// and W is even).  Returns the number of valid rows in this warp.
+template <typename T, int W, bool kVec>
+__device__ __forceinline__ int warp_stage(const T* __restrict__ A, int64_t n, int64_t row0,
+                                          T* sm) {
+  const int lane = threadIdx.x & 31;
+  int64_t rem = n - row0;
+  int rows = rem < 32 ? (int)rem : 32;
+  const int nel = rows * W;
+  const T* src = A + row0 * W;
+  if (kVec) {
+    using V = typename Vec2<T>::type;
+    const V* s2 = reinterpret_cast<const V*>(src);
+    V* d2 = reinterpret_cast<V*>(sm);
+#pragma unroll
+    for (int t = 0; t < W / 2; t++) {
+      int j = lane + 32 * t;
+      if (2 * j < nel) d2[j] = __ldg(s2 + j);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < W; t++) {
+      int j = lane + 32 * t;
+      if (j < nel) sm[j] = __ldg(src + j);
+    }
+  }
+  __syncwarp();
+  return rows;
+}
+
+// ---- fused diagonalize3 -----------------------------------------------------
+template <typename T, bool kVec, bool kReport>
+__global__ void __launch_bounds__(kThreads) eig3_kernel(const T* __restrict__ A, int64_t n,
+                                                        T* __restrict__ lam, T* __restrict__ ang,
+                                                        uint8_t* __restrict__ status,
+                                                        double* __restrict__ report,
+                                                        double* __restrict__ dmat) {
+  __shared__ __align__(16) T sm[kWarps][32 * 6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * 32;
+  if (row0 >= n) return;
+  const int rows = warp_stage<T, 6, kVec>(A, n, row0, sm[warp]);
+  if (lane >= rows) return;
+  const int64_t i = row0 + lane;
+  const T* p = sm[warp] + 6 * lane;
+  sd::Sym3 a;
+  a.a11 = (double)p[0];
+  a.a12 = (double)p[1];
+  a.a13 = (double)p[2];
+  a.a22 = (double)p[3];
+  a.a23 = (double)p[4];
+  a.a33 = (double)p[5];
+  sd::Result3<kReport> r;
+  sd::diagonalize3<kReport>(a, r);
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    lam[3 * i + k] = (T)r.lam[k];
+    ang[3 * i + k] = (T)r.phi[k];
+  }
+  status[i] = r.status;
+  if (kReport) {
+    if (report) {
+      double* rp = report + SD_REPORT_STRIDE * i;
+      const bool err = (r.status & SD_CODE_MASK) >= SD_ERR_FIRST;
+      rp[0] = err ? sd::qnan() : r.ar.n1;
+      rp[1] = err ? sd::qnan() : r.ar.n2;
+      rp[2] = err ? sd::qnan() : r.recon;
+      const int nc = err ? 0 : r.ar.ncand;
+      rp[3] = (double)nc;
+      for (int k = 0; k < 4; k++)
+        for (int j = 0; j < 5; j++) rp[4 + 5 * k + j] = (k < nc) ? r.ar.cand[k][j] : sd::qnan();
+    }
+    if (dmat) {
+#pragma unroll
+      for (int k = 0; k < 9; k++) dmat[9 * i + k] = r.d[k];
+    }
+  }
+}
+
+// ---- fused diagonalize2 -----------------------------------------------------
+template <bool kVec, bool kReport>
+__global__ void __launch_bounds__(kThreads) eig2_kernel(const double* __restrict__ A, int64_t n,
+                                                        double* __restrict__ lam,
+                                                        double* __restrict__ phi,
+                                                        uint8_t* __restrict__ status,
+                                                        double* __restrict__ dmat) {
+  __shared__ __align__(16) double sm[kWarps][32 * 3 + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * 32;
+  if (row0 >= n) return;
+  // 3 values per row: odd width, so stage element-wise (still coalesced)
+  const int rows = warp_stage<double, 3, false>(A, n, row0, sm[warp]);
+  (void)kVec;
+  double l1 = 0.0, l2 = 0.0, ph = 0.0;
+  uint8_t st = 0;
+  if (lane < rows) {
+    const double* p = sm[warp] + 3 * lane;
+    st = sd::diagonalize2(p[0], p[1], p[2], l1, l2, ph);
+  }
+  __syncwarp();
+  // stage (l1, l2) for a coalesced store of the [rows][2] block
+  double* so = sm[warp];
+  if (lane < rows) {
+    so[2 * lane] = l1;
+    so[2 * lane + 1] = l2;
+  }
+  __syncwarp();
+  double* dst = lam + 2 * row0;
+  for (int j = lane; j < 2 * rows; j += 32) dst[j] = so[j];
+  if (lane < rows) {
+    const int64_t i = row0 + lane;
+    phi[i] = ph;
+    status[i] = st;
+    if (kReport && dmat) {
+      double c = sd::qnan(), s = sd::qnan();
+      if (st == SD_CODE_GENERIC) sincos(ph, &s, &c);
+      dmat[4 * i + 0] = c;
+      dmat[4 * i + 1] = -s;
+      dmat[4 * i + 2] = s;
+      dmat[4 * i + 3] = c;
+    }
+  }
+}
+
+// ---- stage kernels (one thread per row, plain loads) -----------------------
+__device__ __forceinline__ int64_t gtid() {
+  return (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+}
+
+__global__ void char_coeffs_kernel(const double* A, int64_t n, double* bcd, uint8_t* status) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  sd::Err e;
+  double b, c, d;
+  if (!sd::finite3(a)) e.raise(SD_ERR_NONFINITE_INPUT);
+  sd::char_coeffs(e, a, b, c, d);
+  bcd[3 * i] = e.code ? sd::qnan() : b;
+  bcd[3 * i + 1] = e.code ? sd::qnan() : c;
+  bcd[3 * i + 2] = e.code ? sd::qnan() : d;
+  status[i] = (uint8_t)e.code;
+}
+
+__global__ void compute_pq_kernel(const double* bcd, int64_t n, double* pqd, uint8_t* status) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Err e;
+  double p = 0, q = 0, delta = 0;
+  bool hd = false;
+  sd::compute_pq(e, bcd[3 * i], bcd[3 * i + 1], bcd[3 * i + 2], p, q, delta, hd);
+  pqd[3 * i] = e.code ? sd::qnan() : p;
+  pqd[3 * i + 1] = e.code ? sd::qnan() : q;
+  pqd[3 * i + 2] = (e.code || !hd) ? sd::qnan() : delta;
+  status[i] = (uint8_t)e.code;
+}
+
+__global__ void eigenvalues3_kernel(const double* bcd, const double* pqd, int64_t n,
+                                    double* lam) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Err e;
+  double l[3];
+  const double delta = pqd[3 * i + 2];
+  sd::eigenvalues3(e, bcd[3 * i], pqd[3 * i], delta, !sd::is_nan(delta), l);
+  lam[3 * i] = l[0];
+  lam[3 * i + 1] = l[1];
+  lam[3 * i + 2] = l[2];
+}
+
+__global__ void pq_expanded_kernel(const double* A, int64_t n, double* pq, uint8_t* status) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  sd::Err e;
+  if (!sd::finite3(a)) e.raise(SD_ERR_NONFINITE_INPUT);
+  double p, q;
+  sd::pq_expanded(e, a, p, q);
+  pq[2 * i] = e.code ? sd::qnan() : p;
+  pq[2 * i + 1] = e.code ? sd::qnan() : q;
+  status[i] = (uint8_t)e.code;
+}
+
+__global__ void compute_v_kernel(const double* A, const double* lam, int64_t n, double* v,
+                                 uint8_t* status) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  double l[3] = {lam[3 * i], lam[3 * i + 1], lam[3 * i + 2]};
+  sd::Err e;
+  double r = sd::compute_v(e, a, l);
+  v[i] = e.code ? sd::qnan() : r;
+  status[i] = (uint8_t)e.code;
+}
+
+__global__ void compute_w_kernel(const double* A, const double* lam, const double* v, int64_t n,
+                                 double* w, uint8_t* status) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  double l[3] = {lam[3 * i], lam[3 * i + 1], lam[3 * i + 2]};
+  sd::Err e;
+  double r = sd::compute_w(e, a, l, v[i]);
+  w[i] = e.code ? sd::qnan() : r;
+  status[i] = (uint8_t)e.code;
+}
+
+__device__ void export_angles(const sd::Err& e, const sd::AngleOut<true>& ar, double* ang,
+                              uint8_t* st, double* rep) {
+  if (e.code) {
+    ang[0] = ang[1] = ang[2] = sd::qnan();
+    *st = (uint8_t)e.code;
+  } else {
+    ang[0] = ar.phi[0];
+    ang[1] = ar.phi[1];
+    ang[2] = ar.phi[2];
+    uint8_t s = 0;
+    if (ar.s2 < 0) s |= SD_FLAG_S2_NEG;
+    if (ar.s3 < 0) s |= SD_FLAG_S3_NEG;
+    if (ar.near_tie) s |= SD_FLAG_NEAR_TIE;
+    *st = s;
+  }
+  if (rep) {
+    rep[0] = ar.n1;
+    rep[1] = ar.n2;
+    rep[2] = sd::qnan();
+    const int nc = e.code ? 0 : ar.ncand;
+    rep[3] = (double)nc;
+    for (int k = 0; k < 4; k++)
+      for (int j = 0; j < 5; j++) rep[4 + 5 * k + j] = (k < nc) ? ar.cand[k][j] : sd::qnan();
+  }
+}
+
+__global__ void resolve_signs_kernel(const double* A, const double* lam, const double* vw,
+                                     int64_t n, double* ang, uint8_t* status, double* report) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  double l[3] = {lam[3 * i], lam[3 * i + 1], lam[3 * i + 2]};
+  sd::Err e;
+  double scale = sd::sym3_scale(e, a);
+  sd::AngleOut<true> ar;
+  if (!e.code) sd::resolve_signs<true>(e, a, scale, l, vw[2 * i], vw[2 * i + 1], ar);
+  export_angles(e, ar, ang + 3 * i, status + i, report ? report + SD_REPORT_STRIDE * i : nullptr);
+}
+
+__global__ void degenerate_double_kernel(const double* A, const double* lam2, int64_t n,
+                                         double* ang, uint8_t* status, double* report) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  sd::Err e;
+  double scale = sd::sym3_scale(e, a);
+  sd::AngleOut<true> ar;
+  if (!e.code) sd::degenerate_double<true>(e, a, scale, lam2[2 * i], lam2[2 * i + 1], ar);
+  export_angles(e, ar, ang + 3 * i, status + i, report ? report + SD_REPORT_STRIDE * i : nullptr);
+}
+
+__global__ void f_vectors_kernel(const double* A, int64_t n, double* f) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Sym3 a = sd::unpack3(A + 6 * i);
+  // f_vectors (eig3.py:209-213)
+  f[4 * i + 0] = a.a12;
+  f[4 * i + 1] = -a.a13;
+  f[4 * i + 2] = a.a22 - a.a33;
+  f[4 * i + 3] = -2.0 * a.a23;
+}
+
+__global__ void g_vectors_kernel(const double* in, int64_t n, double* g) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  // g_vectors (eig3.py:216-225)
+  const double* x = in + 7 * i;
+  const double l1 = x[0], l2 = x[1], l3 = x[2], phi2 = x[3], phi3 = x[4], v = x[5], w = x[6];
+  const double s2phi2 = sin(2.0 * phi2);
+  const double s2phi3 = sin(2.0 * phi3);
+  g[4 * i + 0] = 0.5 * (l1 - l2) * cos(phi2) * s2phi3;
+  g[4 * i + 1] = 0.5 * ((l1 - l2) * w + l2 - l3) * s2phi2;
+  g[4 * i + 2] = (l1 - l2) * (1.0 + (v - 2.0) * w) + (l2 - l3) * v;
+  g[4 * i + 3] = (l1 - l2) * sin(phi2) * s2phi3;
+}
+
+__global__ void compose_rotation_kernel(const double* ang, int64_t n, double* d) {
+  int64_t i = gtid();
+  if (i >= n) return;
+  sd::Err e;
+  double phi[3] = {ang[3 * i], ang[3 * i + 1], ang[3 * i + 2]};
+  double m[9];
+  sd::compose_rotation(e, phi, m);
+  for (int k = 0; k < 9; k++) d[9 * i + k] = m[k];
+}
+
+// DFMA throughput probe: 16 independent chains per thread keep the FP64
+// pipe saturated regardless of its latency.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(int iters, double* sink) {
+  double x[16];
+  const double a = 1.0000001 + threadIdx.x * 1e-12, b = -1e-9;
+#pragma unroll
+  for (int k = 0; k < 16; k++) x[k] = (double)(k + 1) * 1e-3 + blockIdx.x * 1e-9;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; k++) s += x[k];
+  sink[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+template <typename T, bool kReport>
+int launch_eig3(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, double* report,
+                double* d, cudaStream_t s) {
+  if (n < 0 || (n > 0 && (!A || !lam || !ang || !status)))
+    return set_err(SD_EINVAL, "sd_eig3: bad argument");
+  if (n == 0) return SD_OK;
+  const unsigned g = grid_for(n);
+  if (aligned(A, 2 * sizeof(T)))
+    eig3_kernel<T, true, kReport><<<g, kThreads, 0, s>>>(A, n, lam, ang, status, report, d);
+  else
+    eig3_kernel<T, false, kReport><<<g, kThreads, 0, s>>>(A, n, lam, ang, status, report, d);
+  return check_launch("eig3_kernel");
+}
+
+template <bool kReport>
+int launch_eig2(const double* A, int64_t n, double* lam, double* phi, uint8_t* status, double* d,
+                cudaStream_t s) {
+  if (n < 0 || (n > 0 && (!A || !lam || !phi || !status)))
+    return set_err(SD_EINVAL, "sd_eig2: bad argument");
+  if (n == 0) return SD_OK;
+  eig2_kernel<false, kReport><<<grid_for(n), kThreads, 0, s>>>(A, n, lam, phi, status, d);
+  return check_launch("eig2_kernel");
+}
+
+inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+#define SIMPLE_LAUNCH(kernel, ...)                                          \
+  do {                                                                      \
+    if (n < 0) return set_err(SD_EINVAL, #kernel ": negative n");          \
+    if (n == 0) return SD_OK;                                               \
+    kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(__VA_ARGS__); \
+    return check_launch(#kernel);                                           \
+  } while (0)
+
+}  // namespace
+
+// ============================ C ABI =========================================
+extern "C" {
+
+int sd_eig2_f64(const double* A, int64_t n, double* lam, double* phi, uint8_t* status,
+                void* stream) {
+  return launch_eig2<false>(A, n, lam, phi, status, nullptr, S(stream));
+}
+
+int sd_eig2_report_f64(const double* A, int64_t n, double* lam, double* phi, uint8_t* status,
+                       double* d, void* stream) {
+  return launch_eig2<true>(A, n, lam, phi, status, d, S(stream));
+}
+
+int sd_eig3_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
+                void* stream) {
+  return launch_eig3<double, false>(A, n, lam, ang, status, nullptr, nullptr, S(stream));
+}
+
+int sd_eig3_f32(const float* A, int64_t n, float* lam, float* ang, uint8_t* status,
+                void* stream) {
+  return launch_eig3<float, false>(A, n, lam, ang, status, nullptr, nullptr, S(stream));
+}
+
+int sd_eig3_report_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
+                       double* report, double* d, void* stream) {
+  return launch_eig3<double, true>(A, n, lam, ang, status, report, d, S(stream));
+}
+
+int sd_char_coeffs_f64(const double* A, int64_t n, double* bcd, uint8_t* status, void* stream) {
+  SIMPLE_LAUNCH(char_coeffs_kernel, A, n, bcd, status);
+}
+int sd_compute_pq_f64(const double* bcd, int64_t n, double* pqd, uint8_t* status, void* stream) {
+  SIMPLE_LAUNCH(compute_pq_kernel, bcd, n, pqd, status);
+}
+int sd_eigenvalues3_f64(const double* bcd, const double* pqd, int64_t n, double* lam,
+                        void* stream) {
+  SIMPLE_LAUNCH(eigenvalues3_kernel, bcd, pqd, n, lam);
+}
+int sd_pq_expanded_f64(const double* A, int64_t n, double* pq, uint8_t* status, void* stream) {
+  SIMPLE_LAUNCH(pq_expanded_kernel, A, n, pq, status);
+}
+int sd_compute_v_f64(const double* A, const double* lam, int64_t n, double* v, uint8_t* status,
+                     void* stream) {
+  SIMPLE_LAUNCH(compute_v_kernel, A, lam, n, v, status);
+}
+int sd_compute_w_f64(const double* A, const double* lam, const double* v, int64_t n, double* w,
+                     uint8_t* status, void* stream) {
+  SIMPLE_LAUNCH(compute_w_kernel, A, lam, v, n, w, status);
+}
+int sd_resolve_signs_f64(const double* A, const double* lam, const double* vw, int64_t n,
+                         double* ang, uint8_t* status, double* report, void* stream) {
+  SIMPLE_LAUNCH(resolve_signs_kernel, A, lam, vw, n, ang, status, report);
+}
+int sd_degenerate_double_f64(const double* A, const double* lam2, int64_t n, double* ang,
+                             uint8_t* status, double* report, void* stream) {
+  SIMPLE_LAUNCH(degenerate_double_kernel, A, lam2, n, ang, status, report);
+}
+int sd_f_vectors_f64(const double* A, int64_t n, double* f, void* stream) {
+  SIMPLE_LAUNCH(f_vectors_kernel, A, n, f);
+}
+int sd_g_vectors_f64(const double* in, int64_t n, double* g, void* stream) {
+  SIMPLE_LAUNCH(g_vectors_kernel, in, n, g);
+}
+int sd_compose_rotation_f64(const double* ang, int64_t n, double* d, void* stream) {
+  SIMPLE_LAUNCH(compose_rotation_kernel, ang, n, d);
+}
+
+int sd_probe_dfma(int blocks, int iters, double* sink, double* dfma_total, void* stream) {
+  if (blocks <= 0 || iters <= 0 || !sink) return set_err(SD_EINVAL, "sd_probe_dfma: bad argument");
+  dfma_probe_kernel<<<blocks, 256, 0, S(stream)>>>(iters, sink);
+  if (dfma_total) *dfma_total = (double)blocks * 256.0 * 16.0 * (double)iters;
+  return check_launch("dfma_probe_kernel");
+}
+
+__attribute__((visibility("hidden"))) void sd_internal_set_error(const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+}
+
+const char* sd_last_error(void) { return g_err; }
+const char* sd_version(void) { return "symdiag_b200 0.1.0 sm_100a"; }
+int64_t sd_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+"""Parity comparator: GPU results vs reference/oracle results on the same rows.
+
+The contract (north_star in BASELINE.json), stated as code:
+  * status code (branch or error) identical;
+  * selected signs identical on Generic / AlreadyDiagonal2D / DoubleRoot;
+  * eigenvalues: |dl| <= 1e-12 * max(1, max|l|)  (normwise, the reference's
+    own scale convention, core.py:68-73);
+  * angles, "away from degeneracies" = Generic/AlreadyDiagonal2D on both
+    sides, not polished on either side, and outside the EDGE WINDOW
+    (|phi2| or |phi3| within 1e-2 of 0 or pi/2, where arccos(sqrt(.))
+    square-root-amplifies 1-ulp libm differences):
+    wrapped difference mod pi <= 1e-10;
+  * edge-window and polished rows: reported separately, bounded loosely;
+  * DoubleRoot / TripleRoot angles: the repeated eigenspace makes them
+    non-unique; gated through the reconstruction residual instead.
+Flags that may legitimately differ are the ones whose deciding quantity
+lies within rounding distance of its threshold: near_tie (TIE_EPS /
+NEAR_TIE_EPS windows) and polished (the 1e-12 residual gate).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+CODE = 0x0F
+S2, S3, NEAR, POL = 0x10, 0x20, 0x40, 0x80
+EIG_TOL = 1e-12
+ANG_TOL = 1e-10
+EDGE_WIN = 1e-2
+
+
+def wrapped_diff(a, b):
+    d = np.remainder(np.asarray(a, np.float64) - np.asarray(b, np.float64), np.pi)
+    return np.minimum(d, np.pi - d)
+
+
+def edge_window(ang):
+    a = np.abs(np.asarray(ang, np.float64))
+    near = lambda x: (x < EDGE_WIN) | (np.abs(x - np.pi / 2) < EDGE_WIN)  # noqa: E731
+    return near(a[:, 1]) | near(a[:, 2])
+
+
+def compare3(ref: dict, got: dict, eig_tol=EIG_TOL, ang_tol=ANG_TOL) -> dict:
+    rs, gs = np.asarray(ref["status"]), np.asarray(got["status"])
+    rc, gc = rs & CODE, gs & CODE
+    n = len(rs)
+    code_ok = rc == gc
+    ok_rows = code_ok & (rc < 8)
+    sign_ok = ((rs ^ gs) & (S2 | S3)) == 0
+    lam_r = np.asarray(ref["lam"], np.float64)
+    lam_g = np.asarray(got["lam"], np.float64)
+    scale = np.maximum(1.0, np.nanmax(np.abs(lam_r), axis=1))
+    lam_err = np.nanmax(np.abs(lam_r - lam_g), axis=1) / scale
+    err_rows = code_ok & (rc >= 8)
+    nan_ok = np.all(np.isnan(lam_g[err_rows])) and np.all(np.isnan(np.asarray(got["ang"])[err_rows]))
+    ang_r = np.asarray(ref["ang"], np.float64)
+    ang_g = np.asarray(got["ang"], np.float64)
+    ang_err = np.nanmax(wrapped_diff(ang_r, ang_g), axis=1)
+    gen = ok_rows & ((rc == 0) | (rc == 1))
+    pol = ((rs | gs) & POL) != 0
+    edge = edge_window(ang_r)
+    strict = gen & ~pol & ~edge
+    out = dict(
+        n=n,
+        code_mismatch=int((~code_ok).sum()),
+        code_mismatch_rows=np.nonzero(~code_ok)[0][:20].tolist(),
+        sign_mismatch=int((~sign_ok & ok_rows & (rc != 3)).sum()),
+        sign_mismatch_rows=np.nonzero(~sign_ok & ok_rows & (rc != 3))[0][:20].tolist(),
+        near_tie_mismatch=int((((rs ^ gs) & NEAR) != 0).sum()),
+        polished_mismatch=int((((rs ^ gs) & POL) != 0).sum()),
+        error_rows=int(err_rows.sum()),
+        error_outputs_nan=bool(nan_ok),
+        lam_max_err=float(np.nanmax(lam_err[ok_rows])) if ok_rows.any() else 0.0,
+        lam_fail=int((lam_err[ok_rows] > eig_tol).sum()),
+        strict_rows=int(strict.sum()),
+        strict_ang_max=float(ang_err[strict].max()) if strict.any() else 0.0,
+        strict_ang_fail=int((ang_err[strict] > ang_tol).sum()),
+        strict_ang_fail_rows=np.nonzero(strict & (ang_err > ang_tol))[0][:20].tolist(),
+        edge_rows=int((gen & ~pol & edge).sum()),
+        edge_ang_max=float(ang_err[gen & ~pol & edge].max()) if (gen & ~pol & edge).any() else 0.0,
+        polished_rows=int((gen & pol).sum()),
+        polished_ang_max=float(ang_err[gen & pol].max()) if (gen & pol).any() else 0.0,
+        degenerate_rows=int((ok_rows & (rc >= 2)).sum()),
+        degenerate_ang_max=float(np.nanmax(ang_err[ok_rows & (rc >= 2)]))
+        if (ok_rows & (rc >= 2)).any() else 0.0,
+    )
+    if "report" in ref and "report" in got and ref["report"] is not None and got["report"] is not None:
+        rr = np.asarray(ref["report"])[:, 2]
+        gr = np.asarray(got["report"])[:, 2]
+        m = ok_rows
+        out["recon_ref_max"] = float(np.nanmax(rr[m])) if m.any() else 0.0
+        out["recon_gpu_max"] = float(np.nanmax(gr[m])) if m.any() else 0.0
+        # GPU decomposition no worse than the reference's beyond rounding
+        worse = gr[m] > np.maximum(4.0 * rr[m], 1e-12)
+        out["recon_worse"] = int(worse.sum())
+    return out
+
+
+def assert_parity(stats: dict, max_code=0, max_sign=0, max_strict_fail=0, edge_tol=1e-7,
+                  polished_tol=1e-6):
+    assert stats["code_mismatch"] <= max_code, stats
+    assert stats["sign_mismatch"] <= max_sign, stats
+    assert stats["error_outputs_nan"], stats
+    assert stats["lam_fail"] == 0, stats
+    assert stats["strict_ang_fail"] <= max_strict_fail, stats
+    assert stats["edge_ang_max"] <= edge_tol, stats
+    assert stats["polished_ang_max"] <= polished_tol, stats
+    if "recon_worse" in stats:
+        assert stats["recon_worse"] == 0, stats
