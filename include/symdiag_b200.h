@@ -168,6 +168,11 @@ int sd_eig2_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
                      double* phi, uint8_t* status);
 
 /* ---- diagnostics --------------------------------------------------------- */
+/* sd_eig3_f64 evaluated entirely in the reference's literal evaluation
+ * order (one thread per row, no fast path, no deferral).  Same outputs up
+ * to the parity tolerance; used to cross-check the fast path.             */
+int sd_eig3_literal_f64(const double* A, int64_t n, double* lam, double* ang,
+                        uint8_t* status, void* cuda_stream);
 /* FP64-pipe peak probe for the roofline denominator: `blocks` x 256 threads,
  * each runs `iters` x 16 independent DFMA chains; *dfma_total receives the
  * DFMA count (time it with events on `cuda_stream`).  sink[blocks*256].     */

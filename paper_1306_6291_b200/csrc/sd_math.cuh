@@ -49,11 +49,17 @@ __device__ __forceinline__ double pow2(Err& e, double x) {
   if (is_inf(r) && is_finite(x)) e.raise(SD_ERR_OVERFLOW);
   return r;
 }
-// x**3, correctly rounded up to a ~2^-104 relative window
+// x**3, correctly rounded up to a ~2^-104 relative window.  When the
+// leading product overflows, the error terms are inf - inf = NaN, so the
+// overflow is detected on the leading product (CPython: OverflowError).
 __device__ __forceinline__ double pow3(Err& e, double x) {
   double h = __dmul_rn(x, x);
   double l = fma(x, x, -h);
   double hi = __dmul_rn(h, x);
+  if (!is_finite(hi)) {
+    if (is_finite(x)) e.raise(SD_ERR_OVERFLOW);
+    return hi;
+  }
   double lo = fma(h, x, -hi) + __dmul_rn(l, x);
   double r = hi + lo;
   if (is_inf(r) && is_finite(x)) e.raise(SD_ERR_OVERFLOW);
@@ -64,8 +70,12 @@ __device__ __forceinline__ double pow6(Err& e, double x) {
   double h = __dmul_rn(x, x);
   double l = fma(x, x, -h);
   double c = __dmul_rn(h, x);
-  double cl = fma(h, x, -c) + __dmul_rn(l, x);  // x^3 = c + cl
   double s = __dmul_rn(c, c);
+  if (!is_finite(s)) {
+    if (is_finite(x)) e.raise(SD_ERR_OVERFLOW);
+    return s;
+  }
+  double cl = fma(h, x, -c) + __dmul_rn(l, x);  // x^3 = c + cl
   double sl = fma(c, c, -s) + 2.0 * __dmul_rn(c, cl);
   double r = s + sl;
   if (is_inf(r) && is_finite(x)) e.raise(SD_ERR_OVERFLOW);

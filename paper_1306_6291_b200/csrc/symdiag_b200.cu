@@ -19,6 +19,7 @@
 #include "../../include/symdiag_b200.h"
 #include "sd_eig2.cuh"
 #include "sd_eig3.cuh"
+#include "sd_fast3.cuh"
 
 namespace {
 
@@ -134,6 +135,153 @@ __global__ void __launch_bounds__(kThreads) eig3_kernel(const T* __restrict__ A,
 #pragma unroll
       for (int k = 0; k < 9; k++) dmat[9 * i + k] = r.d[k];
     }
+  }
+}
+
+// ---- fast two-phase diagonalize3 (sd_fast3.cuh) -----------------------------
+// Phase A: every thread classifies its row (invariants, p/q, eigenvalues);
+//   triple roots finish here, anything unusual is marked deferred.
+// Phase B: Generic rows of the whole block are compacted through shared
+//   memory so the long fast path runs on dense warps (the degenerate-stress
+//   config is 1/3 generic, randomly interleaved).
+constexpr int kFastThreads = 256;
+
+template <typename T, bool kVec>
+__global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __restrict__ A,
+                                                                 int64_t n, T* __restrict__ lam,
+                                                                 T* __restrict__ ang,
+                                                                 uint8_t* __restrict__ status) {
+  constexpr int W = kFastThreads / 32;
+  __shared__ __align__(16) T stage[W][32 * 6];
+  __shared__ double qa[6][kFastThreads];
+  __shared__ double ql[3][kFastThreads];
+  __shared__ double qs[kFastThreads];
+  __shared__ int qrow[kFastThreads];
+  __shared__ int qcount;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) qcount = 0;
+  __syncthreads();
+  const int64_t row0 = ((int64_t)blockIdx.x * W + warp) * 32;
+  bool generic = false;
+  sd::Sym3 a;
+  double l[3], scale = 1.0;
+  int64_t i = row0 + lane;
+  if (row0 < n) {
+    const int rows = warp_stage<T, 6, kVec>(A, n, row0, stage[warp]);
+    if (lane < rows) {
+      const T* p = stage[warp] + 6 * lane;
+      a.a11 = (double)p[0];
+      a.a12 = (double)p[1];
+      a.a13 = (double)p[2];
+      a.a22 = (double)p[3];
+      a.a23 = (double)p[4];
+      a.a33 = (double)p[5];
+      const int cls = sd::classify3(a, l, scale);
+      if (cls == 1) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          lam[3 * i + k] = (T)l[k];
+          ang[3 * i + k] = (T)0.0;
+        }
+        status[i] = SD_CODE_TRIPLE_ROOT;
+      } else if (cls == 2) {
+        status[i] = sd::kDeferred;
+      } else {
+        generic = true;
+      }
+    }
+  }
+  // warp-aggregated push of generic rows into the block queue
+  const unsigned mask = __ballot_sync(0xffffffffu, generic);
+  int base = 0;
+  if (lane == 0 && mask) base = atomicAdd(&qcount, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (generic) {
+    const int slot = base + __popc(mask & ((1u << lane) - 1u));
+    qa[0][slot] = a.a11;
+    qa[1][slot] = a.a12;
+    qa[2][slot] = a.a13;
+    qa[3][slot] = a.a22;
+    qa[4][slot] = a.a23;
+    qa[5][slot] = a.a33;
+    ql[0][slot] = l[0];
+    ql[1][slot] = l[1];
+    ql[2][slot] = l[2];
+    qs[slot] = scale;
+    qrow[slot] = (int)(i - (int64_t)blockIdx.x * kFastThreads);
+  }
+  __syncthreads();
+  if (tid >= qcount) return;
+  sd::Sym3 g;
+  g.a11 = qa[0][tid];
+  g.a12 = qa[1][tid];
+  g.a13 = qa[2][tid];
+  g.a22 = qa[3][tid];
+  g.a23 = qa[4][tid];
+  g.a33 = qa[5][tid];
+  double gl[3] = {ql[0][tid], ql[1][tid], ql[2][tid]};
+  const int64_t r = (int64_t)blockIdx.x * kFastThreads + qrow[tid];
+  double phi[3];
+  uint8_t st = 0;
+  if (sd::fast_generic(g, qs[tid], gl, phi, st)) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      lam[3 * r + k] = (T)gl[k];
+      ang[3 * r + k] = (T)phi[k];
+    }
+    status[r] = st;
+  } else {
+    status[r] = sd::kDeferred;
+  }
+}
+
+// Deferred rows: every row left with status kDeferred by the fast kernel
+// goes through the literal solver (sd_eig3.cuh).  Each block scans a tile
+// of status bytes, compacts the deferred rows in shared memory and runs
+// them on dense warps.
+constexpr int kDeferTile = 2048;
+
+template <typename T>
+__global__ void __launch_bounds__(256) eig3_deferred_kernel(const T* __restrict__ A, int64_t n,
+                                                            T* __restrict__ lam,
+                                                            T* __restrict__ ang,
+                                                            uint8_t* __restrict__ status) {
+  __shared__ int list[kDeferTile];
+  __shared__ int cnt;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kDeferTile;
+#pragma unroll
+  for (int k = 0; k < kDeferTile / 256; k++) {
+    const int j = k * 256 + tid;
+    const bool d = (base + j < n) && status[base + j] == sd::kDeferred;
+    const unsigned m = __ballot_sync(0xffffffffu, d);
+    int b = 0;
+    if (lane == 0 && m) b = atomicAdd(&cnt, __popc(m));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (d) list[b + __popc(m & ((1u << lane) - 1u))] = j;
+  }
+  __syncthreads();
+  const int c = cnt;
+  for (int k = tid; k < c; k += 256) {
+    const int64_t i = base + list[k];
+    const T* p = A + 6 * i;
+    sd::Sym3 a;
+    a.a11 = (double)p[0];
+    a.a12 = (double)p[1];
+    a.a13 = (double)p[2];
+    a.a22 = (double)p[3];
+    a.a23 = (double)p[4];
+    a.a33 = (double)p[5];
+    sd::Result3<false> r;
+    sd::diagonalize3<false>(a, r);
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      lam[3 * i + q] = (T)r.lam[q];
+      ang[3 * i + q] = (T)r.phi[q];
+    }
+    status[i] = r.status;
   }
 }
 
@@ -383,6 +531,24 @@ int launch_eig3(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, double* 
   return check_launch("eig3_kernel");
 }
 
+// Hot path: fast two-phase kernel, then the deferred-row kernel.
+template <typename T>
+int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cudaStream_t s) {
+  if (n < 0 || (n > 0 && (!A || !lam || !ang || !status)))
+    return set_err(SD_EINVAL, "sd_eig3: bad argument");
+  if (n == 0) return SD_OK;
+  const unsigned g1 = (unsigned)((n + kFastThreads - 1) / kFastThreads);
+  if (aligned(A, 2 * sizeof(T)))
+    eig3_fast_kernel<T, true><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
+  else
+    eig3_fast_kernel<T, false><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
+  int rc = check_launch("eig3_fast_kernel");
+  if (rc != SD_OK) return rc;
+  const unsigned g2 = (unsigned)((n + kDeferTile - 1) / kDeferTile);
+  eig3_deferred_kernel<T><<<g2, 256, 0, s>>>(A, n, lam, ang, status);
+  return check_launch("eig3_deferred_kernel");
+}
+
 template <bool kReport>
 int launch_eig2(const double* A, int64_t n, double* lam, double* phi, uint8_t* status, double* d,
                 cudaStream_t s) {
@@ -420,12 +586,17 @@ int sd_eig2_report_f64(const double* A, int64_t n, double* lam, double* phi, uin
 
 int sd_eig3_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
                 void* stream) {
+  return launch_eig3_fast<double>(A, n, lam, ang, status, S(stream));
+}
+
+int sd_eig3_literal_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
+                        void* stream) {
   return launch_eig3<double, false>(A, n, lam, ang, status, nullptr, nullptr, S(stream));
 }
 
 int sd_eig3_f32(const float* A, int64_t n, float* lam, float* ang, uint8_t* status,
                 void* stream) {
-  return launch_eig3<float, false>(A, n, lam, ang, status, nullptr, nullptr, S(stream));
+  return launch_eig3_fast<float>(A, n, lam, ang, status, S(stream));
 }
 
 int sd_eig3_report_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
