@@ -157,12 +157,15 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   __shared__ double ql[3][kFastThreads];
   __shared__ double qs[kFastThreads];
   __shared__ int qrow[kFastThreads];
-  __shared__ int qcount;
+  __shared__ int qgen, qdbl;  // generic rows fill the queue from the front, double roots from the back
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) qcount = 0;
+  if (tid == 0) {
+    qgen = 0;
+    qdbl = 0;
+  }
   __syncthreads();
   const int64_t row0 = ((int64_t)blockIdx.x * W + warp) * 32;
-  bool generic = false;
+  int cls = 2;
   sd::Sym3 a;
   double l[3], scale = 1.0;
   int64_t i = row0 + lane;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
       a.a22 = (double)p[3];
       a.a23 = (double)p[4];
       a.a33 = (double)p[5];
-      const int cls = sd::classify3(a, l, scale);
+      cls = sd::classify3(a, l, scale);
       if (cls == 1) {
 #pragma unroll
         for (int k = 0; k < 3; k++) {
@@ -186,18 +189,24 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
         status[i] = SD_CODE_TRIPLE_ROOT;
       } else if (cls == 2) {
         status[i] = sd::kDeferred;
-      } else {
-        generic = true;
       }
     }
   }
-  // warp-aggregated push of generic rows into the block queue
-  const unsigned mask = __ballot_sync(0xffffffffu, generic);
-  int base = 0;
-  if (lane == 0 && mask) base = atomicAdd(&qcount, __popc(mask));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (generic) {
-    const int slot = base + __popc(mask & ((1u << lane) - 1u));
+  // warp-aggregated push into the block queue: generic rows at the front,
+  // double roots at the back, so phase-B warps are (almost) homogeneous
+  const unsigned mg = __ballot_sync(0xffffffffu, cls == 0);
+  const unsigned md = __ballot_sync(0xffffffffu, cls == 3);
+  int bg = 0, bd = 0;
+  if (lane == 0) {
+    if (mg) bg = atomicAdd(&qgen, __popc(mg));
+    if (md) bd = atomicAdd(&qdbl, __popc(md));
+  }
+  bg = __shfl_sync(0xffffffffu, bg, 0);
+  bd = __shfl_sync(0xffffffffu, bd, 0);
+  const unsigned below = (1u << lane) - 1u;
+  if (cls == 0 || cls == 3) {
+    const int slot = (cls == 0) ? bg + __popc(mg & below)
+                                : kFastThreads - 1 - (bd + __popc(md & below));
     qa[0][slot] = a.a11;
     qa[1][slot] = a.a12;
     qa[2][slot] = a.a13;
@@ -211,7 +220,8 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
     qrow[slot] = (int)(i - (int64_t)blockIdx.x * kFastThreads);
   }
   __syncthreads();
-  if (tid >= qcount) return;
+  const bool is_gen = tid < qgen;
+  if (!is_gen && tid < kFastThreads - qdbl) return;
   sd::Sym3 g;
   g.a11 = qa[0][tid];
   g.a12 = qa[1][tid];
@@ -223,7 +233,9 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   const int64_t r = (int64_t)blockIdx.x * kFastThreads + qrow[tid];
   double phi[3];
   uint8_t st = 0;
-  if (sd::fast_generic(g, qs[tid], gl, phi, st)) {
+  const bool done = is_gen ? sd::fast_generic(g, qs[tid], gl, phi, st)
+                           : sd::fast_double(g, qs[tid], gl, phi, st);
+  if (done) {
 #pragma unroll
     for (int k = 0; k < 3; k++) {
       lam[3 * r + k] = (T)gl[k];
