@@ -635,6 +635,33 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
   return best;
 }
 
+// The tail of diagonalize3 (eig3.py:553-561) for a row whose closed-form
+// (lam, phi) are known: literal residual, polish if above the gate, accept
+// if better.  Returns true when the polished angles were accepted (phi
+// updated).  Non-finite polished angles set phi[0] = NaN (NonFiniteInput is
+// raised by Angles3 whether or not the polish is accepted, core.py:127).
+__device__ __noinline__ bool polish_rows_literal(const Sym3& a, const double lam[3],
+                                                 double phi[3]) {
+  Err e;
+  const double scale = sym3_scale(e, a);
+  double d[9];
+  compose_rotation(e, phi, d);
+  const double recon_res = abs_residual(d, lam, a) / scale;
+  if (!(recon_res > 1e-12)) return false;
+  double phis[3] = {phi[0], phi[1], phi[2]};
+  const double abs_res = polish_angles(a, lam, phis, scale);
+  if (!is_finite(phis[0]) || !is_finite(phis[1]) || !is_finite(phis[2])) {
+    phi[0] = qnan();
+    return false;
+  }
+  if (abs_res / scale < recon_res) {
+#pragma unroll
+    for (int i = 0; i < 3; i++) phi[i] = wrap_half_pi(e, phis[i]);
+    return true;
+  }
+  return false;
+}
+
 // ---- diagonalize3 (eig3.py:509-565) ---------------------------------------
 template <bool kReport>
 struct Result3 {

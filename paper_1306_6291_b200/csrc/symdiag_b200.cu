@@ -146,6 +146,18 @@ __global__ void __launch_bounds__(kThreads) eig3_kernel(const T* __restrict__ A,
 //   config is 1/3 generic, randomly interleaved).
 constexpr int kFastThreads = 256;
 
+template <typename T>
+__device__ __forceinline__ sd::Sym3 load_row(const T* p) {
+  sd::Sym3 a;
+  a.a11 = (double)p[0];
+  a.a12 = (double)p[1];
+  a.a13 = (double)p[2];
+  a.a22 = (double)p[3];
+  a.a23 = (double)p[4];
+  a.a33 = (double)p[5];
+  return a;
+}
+
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
@@ -180,13 +192,15 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
       a.a23 = (double)p[4];
       a.a33 = (double)p[5];
       cls = sd::classify3(a, l, scale);
-      if (cls == 1) {
+      if (cls == 1 || cls == 4) {
 #pragma unroll
         for (int k = 0; k < 3; k++) {
           lam[3 * i + k] = (T)l[k];
           ang[3 * i + k] = (T)0.0;
         }
-        status[i] = SD_CODE_TRIPLE_ROOT;
+        // fp32 outputs cannot carry the closed form into the polish: literal
+        status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT
+                               : (sizeof(T) == 8 ? sd::kPolishTriple : sd::kDeferred);
       } else if (cls == 2) {
         status[i] = sd::kDeferred;
       }
@@ -233,9 +247,10 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   const int64_t r = (int64_t)blockIdx.x * kFastThreads + qrow[tid];
   double phi[3];
   uint8_t st = 0;
-  const bool done = is_gen ? sd::fast_generic(g, qs[tid], gl, phi, st)
-                           : sd::fast_double(g, qs[tid], gl, phi, st);
-  if (done) {
+  const int rc = is_gen ? sd::fast_generic(g, qs[tid], gl, phi, st)
+                        : sd::fast_double(g, qs[tid], gl, phi, st);
+  if (rc == sd::kFastDone || (rc == sd::kFastPolish && sizeof(T) == 8)) {
+    // done, or (fp64) closed form written with the polish pending
 #pragma unroll
     for (int k = 0; k < 3; k++) {
       lam[3 * r + k] = (T)gl[k];
@@ -247,45 +262,53 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   }
 }
 
-// Deferred rows: every row left with status kDeferred by the fast kernel
-// goes through the literal solver (sd_eig3.cuh).  Each block scans a tile
-// of status bytes, compacts the deferred rows in shared memory and runs
-// them on dense warps.
-constexpr int kDeferTile = 2048;
+// Fix-up pass after the fast kernel.  Each block scans a tile of status
+// bytes and compacts two lists in shared memory: rows marked kDeferred are
+// recomputed by the literal solver (sd_eig3.cuh); rows marked kPolish* keep
+// their closed-form result and only run the Gauss-Newton polish
+// (eig3.py:553-561).  Both lists run on dense warps, one after the other.
+constexpr int kFixTile = 1024;
+constexpr int kFixThreads = 128;
 
 template <typename T>
-__global__ void __launch_bounds__(256) eig3_deferred_kernel(const T* __restrict__ A, int64_t n,
-                                                            T* __restrict__ lam,
-                                                            T* __restrict__ ang,
-                                                            uint8_t* __restrict__ status) {
-  __shared__ int list[kDeferTile];
-  __shared__ int cnt;
+__global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __restrict__ A,
+                                                                 int64_t n, T* __restrict__ lam,
+                                                                 T* __restrict__ ang,
+                                                                 uint8_t* __restrict__ status) {
+  __shared__ short lit[kFixTile];
+  __shared__ short pol[kFixTile];
+  __shared__ int nlit, npol;
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) cnt = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kDeferTile;
-#pragma unroll
-  for (int k = 0; k < kDeferTile / 256; k++) {
-    const int j = k * 256 + tid;
-    const bool d = (base + j < n) && status[base + j] == sd::kDeferred;
-    const unsigned m = __ballot_sync(0xffffffffu, d);
-    int b = 0;
-    if (lane == 0 && m) b = atomicAdd(&cnt, __popc(m));
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (d) list[b + __popc(m & ((1u << lane) - 1u))] = j;
+  if (tid == 0) {
+    nlit = 0;
+    npol = 0;
   }
   __syncthreads();
-  const int c = cnt;
-  for (int k = tid; k < c; k += 256) {
-    const int64_t i = base + list[k];
-    const T* p = A + 6 * i;
-    sd::Sym3 a;
-    a.a11 = (double)p[0];
-    a.a12 = (double)p[1];
-    a.a13 = (double)p[2];
-    a.a22 = (double)p[3];
-    a.a23 = (double)p[4];
-    a.a33 = (double)p[5];
+  const int64_t base = (int64_t)blockIdx.x * kFixTile;
+#pragma unroll
+  for (int k = 0; k < kFixTile / kFixThreads; k++) {
+    const int j = k * kFixThreads + tid;
+    const int code = (base + j < n) ? (status[base + j] & SD_CODE_MASK) : 0;
+    const bool dl = code == sd::kDeferred;
+    const bool dp = code > sd::kDeferred && code < SD_ERR_FIRST;
+    const unsigned ml = __ballot_sync(0xffffffffu, dl);
+    const unsigned mp = __ballot_sync(0xffffffffu, dp);
+    int bl = 0, bp = 0;
+    if (lane == 0) {
+      if (ml) bl = atomicAdd(&nlit, __popc(ml));
+      if (mp) bp = atomicAdd(&npol, __popc(mp));
+    }
+    bl = __shfl_sync(0xffffffffu, bl, 0);
+    bp = __shfl_sync(0xffffffffu, bp, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (dl) lit[bl + __popc(ml & below)] = (short)j;
+    if (dp) pol[bp + __popc(mp & below)] = (short)j;
+  }
+  __syncthreads();
+  const int cl = nlit, cp = npol;
+  for (int k = tid; k < cl; k += kFixThreads) {
+    const int64_t i = base + lit[k];
+    sd::Sym3 a = load_row(A + 6 * i);
     sd::Result3<false> r;
     sd::diagonalize3<false>(a, r);
 #pragma unroll
@@ -294,6 +317,28 @@ __global__ void __launch_bounds__(256) eig3_deferred_kernel(const T* __restrict_
       ang[3 * i + q] = (T)r.phi[q];
     }
     status[i] = r.status;
+  }
+  for (int k = tid; k < cp; k += kFixThreads) {
+    const int64_t i = base + pol[k];
+    const sd::Sym3 a = load_row(A + 6 * i);
+    const uint8_t st = status[i];
+    double lm[3] = {(double)lam[3 * i], (double)lam[3 * i + 1], (double)lam[3 * i + 2]};
+    double ph[3] = {(double)ang[3 * i], (double)ang[3 * i + 1], (double)ang[3 * i + 2]};
+    uint8_t code = SD_CODE_GENERIC;
+    if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
+    if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
+    uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
+    if (sd::polish_rows_literal(a, lm, ph)) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
+      out |= SD_FLAG_POLISHED;
+    }
+    if (ph[0] != ph[0]) {  // non-finite polished angles: NonFiniteInput (core.py:127)
+#pragma unroll
+      for (int q = 0; q < 3; q++) lam[3 * i + q] = ang[3 * i + q] = (T)sd::qnan();
+      out = SD_ERR_NONFINITE_INPUT;
+    }
+    status[i] = out;
   }
 }
 
@@ -556,9 +601,9 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
     eig3_fast_kernel<T, false><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
   int rc = check_launch("eig3_fast_kernel");
   if (rc != SD_OK) return rc;
-  const unsigned g2 = (unsigned)((n + kDeferTile - 1) / kDeferTile);
-  eig3_deferred_kernel<T><<<g2, 256, 0, s>>>(A, n, lam, ang, status);
-  return check_launch("eig3_deferred_kernel");
+  const unsigned g2 = (unsigned)((n + kFixTile - 1) / kFixTile);
+  eig3_fixup_kernel<T><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
+  return check_launch("eig3_fixup_kernel");
 }
 
 template <bool kReport>
