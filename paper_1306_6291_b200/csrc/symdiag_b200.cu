@@ -262,83 +262,76 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   }
 }
 
-// Fix-up pass after the fast kernel.  Each block scans a tile of status
-// bytes and compacts two lists in shared memory: rows marked kDeferred are
-// recomputed by the literal solver (sd_eig3.cuh); rows marked kPolish* keep
-// their closed-form result and only run the Gauss-Newton polish
-// (eig3.py:553-561).  Both lists run on dense warps, one after the other.
+// Fix-up passes after the fast kernel.  Each block scans a tile of status
+// bytes and compacts the rows it owns in shared memory so they run on dense
+// warps:
+//   kPolish = true : rows marked kPolish* keep their closed-form result and
+//                    only run the Gauss-Newton tail (polish_compact);
+//   kPolish = false: rows marked kDeferred are recomputed by the literal
+//                    solver (sd_eig3.cuh).
+// Two separate launches keep each kernel's code small (the literal solver
+// is ~13k SASS instructions; mixing it with the polish thrashed the
+// instruction cache, profiles/r1_*).
 constexpr int kFixTile = 1024;
 constexpr int kFixThreads = 128;
 
-template <typename T>
+template <typename T, bool kPolish>
 __global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
                                                                  uint8_t* __restrict__ status) {
-  __shared__ short lit[kFixTile];
-  __shared__ short pol[kFixTile];
-  __shared__ int nlit, npol;
+  __shared__ short list[kFixTile];
+  __shared__ int cnt;
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) {
-    nlit = 0;
-    npol = 0;
-  }
+  if (tid == 0) cnt = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kFixTile;
 #pragma unroll
   for (int k = 0; k < kFixTile / kFixThreads; k++) {
     const int j = k * kFixThreads + tid;
     const int code = (base + j < n) ? (status[base + j] & SD_CODE_MASK) : 0;
-    const bool dl = code == sd::kDeferred;
-    const bool dp = code > sd::kDeferred && code < SD_ERR_FIRST;
-    const unsigned ml = __ballot_sync(0xffffffffu, dl);
-    const unsigned mp = __ballot_sync(0xffffffffu, dp);
-    int bl = 0, bp = 0;
-    if (lane == 0) {
-      if (ml) bl = atomicAdd(&nlit, __popc(ml));
-      if (mp) bp = atomicAdd(&npol, __popc(mp));
-    }
-    bl = __shfl_sync(0xffffffffu, bl, 0);
-    bp = __shfl_sync(0xffffffffu, bp, 0);
-    const unsigned below = (1u << lane) - 1u;
-    if (dl) lit[bl + __popc(ml & below)] = (short)j;
-    if (dp) pol[bp + __popc(mp & below)] = (short)j;
+    const bool mine = kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST)
+                              : (code == sd::kDeferred);
+    const unsigned m = __ballot_sync(0xffffffffu, mine);
+    int b = 0;
+    if (lane == 0 && m) b = atomicAdd(&cnt, __popc(m));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (mine) list[b + __popc(m & ((1u << lane) - 1u))] = (short)j;
   }
   __syncthreads();
-  const int cl = nlit, cp = npol;
-  for (int k = tid; k < cl; k += kFixThreads) {
-    const int64_t i = base + lit[k];
-    sd::Sym3 a = load_row(A + 6 * i);
-    sd::Result3<false> r;
-    sd::diagonalize3<false>(a, r);
-#pragma unroll
-    for (int q = 0; q < 3; q++) {
-      lam[3 * i + q] = (T)r.lam[q];
-      ang[3 * i + q] = (T)r.phi[q];
-    }
-    status[i] = r.status;
-  }
-  for (int k = tid; k < cp; k += kFixThreads) {
-    const int64_t i = base + pol[k];
+  const int c = cnt;
+  for (int k = tid; k < c; k += kFixThreads) {
+    const int64_t i = base + list[k];
     const sd::Sym3 a = load_row(A + 6 * i);
-    const uint8_t st = status[i];
-    double lm[3] = {(double)lam[3 * i], (double)lam[3 * i + 1], (double)lam[3 * i + 2]};
-    double ph[3] = {(double)ang[3 * i], (double)ang[3 * i + 1], (double)ang[3 * i + 2]};
-    uint8_t code = SD_CODE_GENERIC;
-    if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
-    if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
-    uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
-    if (sd::polish_rows_literal(a, lm, ph)) {
+    if (!kPolish) {
+      sd::Result3<false> r;
+      sd::diagonalize3<false>(a, r);
 #pragma unroll
-      for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
-      out |= SD_FLAG_POLISHED;
-    }
-    if (ph[0] != ph[0]) {  // non-finite polished angles: NonFiniteInput (core.py:127)
+      for (int q = 0; q < 3; q++) {
+        lam[3 * i + q] = (T)r.lam[q];
+        ang[3 * i + q] = (T)r.phi[q];
+      }
+      status[i] = r.status;
+    } else {
+      const uint8_t st = status[i];
+      const double lm[3] = {(double)lam[3 * i], (double)lam[3 * i + 1], (double)lam[3 * i + 2]};
+      double ph[3] = {(double)ang[3 * i], (double)ang[3 * i + 1], (double)ang[3 * i + 2]};
+      uint8_t code = SD_CODE_GENERIC;
+      if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
+      if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
+      uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
+      if (sd::polish_compact(a, lm, ph)) {
 #pragma unroll
-      for (int q = 0; q < 3; q++) lam[3 * i + q] = ang[3 * i + q] = (T)sd::qnan();
-      out = SD_ERR_NONFINITE_INPUT;
+        for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
+        out |= SD_FLAG_POLISHED;
+      }
+      if (ph[0] != ph[0]) {  // non-finite polished angles: NonFiniteInput (core.py:127)
+#pragma unroll
+        for (int q = 0; q < 3; q++) lam[3 * i + q] = ang[3 * i + q] = (T)sd::qnan();
+        out = SD_ERR_NONFINITE_INPUT;
+      }
+      status[i] = out;
     }
-    status[i] = out;
   }
 }
 
@@ -602,8 +595,11 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   int rc = check_launch("eig3_fast_kernel");
   if (rc != SD_OK) return rc;
   const unsigned g2 = (unsigned)((n + kFixTile - 1) / kFixTile);
-  eig3_fixup_kernel<T><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
-  return check_launch("eig3_fixup_kernel");
+  eig3_fixup_kernel<T, true><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
+  rc = check_launch("eig3_polish_kernel");
+  if (rc != SD_OK) return rc;
+  eig3_fixup_kernel<T, false><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
+  return check_launch("eig3_literal_kernel");
 }
 
 template <bool kReport>
