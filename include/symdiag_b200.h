@@ -173,6 +173,12 @@ int sd_eig2_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
  * to the parity tolerance; used to cross-check the fast path.             */
 int sd_eig3_literal_f64(const double* A, int64_t n, double* lam, double* ang,
                         uint8_t* status, void* cuda_stream);
+/* Only the first (fast, classifying) pass of sd_eig3_f64: rows it could not
+ * finish keep internal codes 4 (deferred to the literal solver; bits 4-7 =
+ * reason, see sd_fast3.cuh) or 5-7 (closed form written, polish pending).
+ * Diagnostics: measures how much of a workload takes the fast path.        */
+int sd_eig3_classify_f64(const double* A, int64_t n, double* lam, double* ang,
+                         uint8_t* status, void* cuda_stream);
 /* FP64-pipe peak probe for the roofline denominator: `blocks` x 256 threads,
  * each runs `iters` x 16 independent DFMA chains; *dfma_total receives the
  * DFMA count (time it with events on `cuda_stream`).  sink[blocks*256].     */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "sd_eig3_f32_host": [_P, _P, _I64, _P, _P, _P],
     "sd_eig2_f64_host": [_P, _P, _I64, _P, _P, _P],
     "sd_eig3_literal_f64": [_P, _I64, _P, _P, _P, _P],
+    "sd_eig3_classify_f64": [_P, _I64, _P, _P, _P, _P],
     "sd_probe_dfma": [_I, _I, _P, ctypes.POINTER(ctypes.c_double), _P],
     "sd_last_error": [],
     "sd_version": [],

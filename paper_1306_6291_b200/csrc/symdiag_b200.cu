@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   }
   __syncthreads();
   const int64_t row0 = ((int64_t)blockIdx.x * W + warp) * 32;
-  int cls = 2;
+  int cls = 2, reason = 0;
   sd::Sym3 a;
   double l[3], scale = 1.0;
   int64_t i = row0 + lane;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
       a.a22 = (double)p[3];
       a.a23 = (double)p[4];
       a.a33 = (double)p[5];
-      cls = sd::classify3(a, l, scale);
+      cls = sd::classify3(a, l, scale, reason);
       if (cls == 1 || cls == 4) {
 #pragma unroll
         for (int k = 0; k < 3; k++) {
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
         status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT
                                : (sizeof(T) == 8 ? sd::kPolishTriple : sd::kDeferred);
       } else if (cls == 2) {
-        status[i] = sd::kDeferred;
+        status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
       }
     }
   }
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
     }
     status[r] = st;
   } else {
-    status[r] = sd::kDeferred;
+    status[r] = (rc == sd::kFastPolish) ? (uint8_t)(sd::kDeferred | (11 << 4)) : st;
   }
 }
 
@@ -640,6 +640,19 @@ int sd_eig2_report_f64(const double* A, int64_t n, double* lam, double* phi, uin
 int sd_eig3_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
                 void* stream) {
   return launch_eig3_fast<double>(A, n, lam, ang, status, S(stream));
+}
+
+int sd_eig3_classify_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
+                         void* stream) {
+  if (n < 0 || (n > 0 && (!A || !lam || !ang || !status)))
+    return set_err(SD_EINVAL, "sd_eig3_classify_f64: bad argument");
+  if (n == 0) return SD_OK;
+  const unsigned g1 = (unsigned)((n + kFastThreads - 1) / kFastThreads);
+  if (aligned(A, 16))
+    eig3_fast_kernel<double, true><<<g1, kFastThreads, 0, S(stream)>>>(A, n, lam, ang, status);
+  else
+    eig3_fast_kernel<double, false><<<g1, kFastThreads, 0, S(stream)>>>(A, n, lam, ang, status);
+  return check_launch("eig3_fast_kernel");
 }
 
 int sd_eig3_literal_f64(const double* A, int64_t n, double* lam, double* ang, uint8_t* status,
