@@ -320,7 +320,12 @@ __global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __rest
       if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
       if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
       uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
-      if (sd::polish_compact(a, lm, ph)) {
+      // the 1e-12 gate on the literal residual (numpy's FMA chains, eig3.py:504-506)
+      sd::Err e;
+      double dm[9];
+      sd::compose_rotation(e, ph, dm);
+      const double rr = sd::abs_residual(dm, lm, a) / sd::sym3_scale(e, a);
+      if (rr > 1e-12 && sd::polish_compact(a, lm, ph)) {
 #pragma unroll
         for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
         out |= SD_FLAG_POLISHED;
