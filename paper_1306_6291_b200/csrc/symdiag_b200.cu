@@ -262,82 +262,109 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
   }
 }
 
-// Fix-up passes after the fast kernel.  Each block scans a tile of status
-// bytes and compacts the rows it owns in shared memory so they run on dense
-// warps:
+// Fix-up passes after the fast kernel:
 //   kPolish = true : rows marked kPolish* keep their closed-form result and
-//                    only run the Gauss-Newton tail (polish_compact);
+//                    only run the Gauss-Newton tail (literal residual gate,
+//                    then polish_compact);
 //   kPolish = false: rows marked kDeferred are recomputed by the literal
 //                    solver (sd_eig3.cuh).
-// Two separate launches keep each kernel's code small (the literal solver
-// is ~13k SASS instructions; mixing it with the polish thrashed the
-// instruction cache, profiles/r1_*).
+// Such rows are sparse (0.02-10% of a batch) and each is expensive, so the
+// kernel is persistent: a grid of ~4 blocks per SM strides over tiles of
+// status bytes, queues the rows it owns in shared memory and runs them only
+// once a full block's worth has accumulated.  Dense warps, no tail of
+// one-row blocks, no global workspace.  Two separate launches keep each
+// kernel's code small (the literal solver is ~13k SASS instructions).
 constexpr int kFixTile = 1024;
 constexpr int kFixThreads = 128;
+constexpr int kFixQueue = kFixTile + kFixThreads;
+
+template <typename T, bool kPolish>
+__device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict__ lam,
+                                          T* __restrict__ ang, uint8_t* __restrict__ status,
+                                          int64_t i) {
+  const sd::Sym3 a = load_row(A + 6 * i);
+  if (!kPolish) {
+    sd::Result3<false> r;
+    sd::diagonalize3<false>(a, r);
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      lam[3 * i + q] = (T)r.lam[q];
+      ang[3 * i + q] = (T)r.phi[q];
+    }
+    status[i] = r.status;
+  } else {
+    const uint8_t st = status[i];
+    const double lm[3] = {(double)lam[3 * i], (double)lam[3 * i + 1], (double)lam[3 * i + 2]};
+    double ph[3] = {(double)ang[3 * i], (double)ang[3 * i + 1], (double)ang[3 * i + 2]};
+    uint8_t code = SD_CODE_GENERIC;
+    if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
+    if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
+    uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
+    // the 1e-12 gate on the literal residual (numpy's FMA chains, eig3.py:504-506)
+    sd::Err e;
+    double dm[9];
+    sd::compose_rotation(e, ph, dm);
+    const double rr = sd::abs_residual(dm, lm, a) / sd::sym3_scale(e, a);
+    if (rr > 1e-12 && sd::polish_compact(a, lm, ph)) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
+      out |= SD_FLAG_POLISHED;
+    }
+    if (ph[0] != ph[0]) {  // non-finite polished angles: NonFiniteInput (core.py:127)
+#pragma unroll
+      for (int q = 0; q < 3; q++) lam[3 * i + q] = ang[3 * i + q] = (T)sd::qnan();
+      out = SD_ERR_NONFINITE_INPUT;
+    }
+    status[i] = out;
+  }
+}
 
 template <typename T, bool kPolish>
 __global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
                                                                  uint8_t* __restrict__ status) {
-  __shared__ short list[kFixTile];
+  __shared__ int64_t queue[kFixQueue];
   __shared__ int cnt;
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) cnt = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kFixTile;
+  const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * kFixTile;
 #pragma unroll
-  for (int k = 0; k < kFixTile / kFixThreads; k++) {
-    const int j = k * kFixThreads + tid;
-    const int code = (base + j < n) ? (status[base + j] & SD_CODE_MASK) : 0;
-    const bool mine = kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST)
-                              : (code == sd::kDeferred);
-    const unsigned m = __ballot_sync(0xffffffffu, mine);
-    int b = 0;
-    if (lane == 0 && m) b = atomicAdd(&cnt, __popc(m));
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (mine) list[b + __popc(m & ((1u << lane) - 1u))] = (short)j;
-  }
-  __syncthreads();
-  const int c = cnt;
-  for (int k = tid; k < c; k += kFixThreads) {
-    const int64_t i = base + list[k];
-    const sd::Sym3 a = load_row(A + 6 * i);
-    if (!kPolish) {
-      sd::Result3<false> r;
-      sd::diagonalize3<false>(a, r);
-#pragma unroll
-      for (int q = 0; q < 3; q++) {
-        lam[3 * i + q] = (T)r.lam[q];
-        ang[3 * i + q] = (T)r.phi[q];
-      }
-      status[i] = r.status;
-    } else {
-      const uint8_t st = status[i];
-      const double lm[3] = {(double)lam[3 * i], (double)lam[3 * i + 1], (double)lam[3 * i + 2]};
-      double ph[3] = {(double)ang[3 * i], (double)ang[3 * i + 1], (double)ang[3 * i + 2]};
-      uint8_t code = SD_CODE_GENERIC;
-      if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
-      if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
-      uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
-      // the 1e-12 gate on the literal residual (numpy's FMA chains, eig3.py:504-506)
-      sd::Err e;
-      double dm[9];
-      sd::compose_rotation(e, ph, dm);
-      const double rr = sd::abs_residual(dm, lm, a) / sd::sym3_scale(e, a);
-      if (rr > 1e-12 && sd::polish_compact(a, lm, ph)) {
-#pragma unroll
-        for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
-        out |= SD_FLAG_POLISHED;
-      }
-      if (ph[0] != ph[0]) {  // non-finite polished angles: NonFiniteInput (core.py:127)
-#pragma unroll
-        for (int q = 0; q < 3; q++) lam[3 * i + q] = ang[3 * i + q] = (T)sd::qnan();
-        out = SD_ERR_NONFINITE_INPUT;
-      }
-      status[i] = out;
+    for (int k = 0; k < kFixTile / kFixThreads; k++) {
+      const int64_t j = base + k * kFixThreads + tid;
+      const int code = (j < n) ? (status[j] & SD_CODE_MASK) : 0;
+      const bool mine = kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST)
+                                : (code == sd::kDeferred);
+      const unsigned m = __ballot_sync(0xffffffffu, mine);
+      int b = 0;
+      if (lane == 0 && m) b = atomicAdd(&cnt, __popc(m));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (mine) queue[b + __popc(m & ((1u << lane) - 1u))] = j;
     }
+    __syncthreads();
+    const int c = cnt;
+    if (c >= kFixThreads) {  // a full block's worth (or more): run them now
+      for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kPolish>(A, lam, ang, status, queue[k]);
+      __syncthreads();
+      if (tid == 0) cnt = 0;
+    }
+    __syncthreads();
   }
+  const int c = cnt;
+  for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kPolish>(A, lam, ang, status, queue[k]);
+}
+
+int fixup_grid(int64_t n) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (nsm <= 0) nsm = 148;
+  const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
+  const int64_t g = (int64_t)nsm * 4;
+  return (int)(ntiles < g ? ntiles : g);
 }
 
 // ---- fused diagonalize2 -----------------------------------------------------
@@ -599,7 +626,7 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
     eig3_fast_kernel<T, false><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
   int rc = check_launch("eig3_fast_kernel");
   if (rc != SD_OK) return rc;
-  const unsigned g2 = (unsigned)((n + kFixTile - 1) / kFixTile);
+  const unsigned g2 = (unsigned)fixup_grid(n);
   eig3_fixup_kernel<T, true><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;
