@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __rest
 // once a full block's worth has accumulated.  Dense warps, no tail of
 // one-row blocks, no global workspace.  Two separate launches keep each
 // kernel's code small (the literal solver is ~13k SASS instructions).
-constexpr int kFixTile = 1024;
+constexpr int kFixTile = 2048;
 constexpr int kFixThreads = 128;
 constexpr int kFixQueue = kFixTile + kFixThreads;
 
@@ -319,11 +319,19 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
   }
 }
 
+// does a status byte belong to this pass?
+template <bool kPolish>
+__device__ __forceinline__ bool fix_mine(unsigned byte) {
+  const unsigned code = byte & SD_CODE_MASK;
+  return kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST) : (code == sd::kDeferred);
+}
+
 template <typename T, bool kPolish>
 __global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
-                                                                 uint8_t* __restrict__ status) {
+                                                                 uint8_t* __restrict__ status,
+                                                                 int vec) {
   __shared__ int64_t queue[kFixQueue];
   __shared__ int cnt;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -331,18 +339,35 @@ __global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __rest
   __syncthreads();
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * kFixTile;
+    // each thread owns kFixTile / kFixThreads = 16 consecutive status bytes:
+    // one 16-byte load when the tile is complete and aligned
+    const int64_t r0 = tile * kFixTile + (int64_t)tid * 16;
+    unsigned mask = 0;
+    if (vec && tile * kFixTile + kFixTile <= n) {
+      const uint4 w = __ldcg(reinterpret_cast<const uint4*>(status + r0));
+      const unsigned words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int k = 0; k < kFixTile / kFixThreads; k++) {
-      const int64_t j = base + k * kFixThreads + tid;
-      const int code = (j < n) ? (status[j] & SD_CODE_MASK) : 0;
-      const bool mine = kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST)
-                                : (code == sd::kDeferred);
-      const unsigned m = __ballot_sync(0xffffffffu, mine);
-      int b = 0;
-      if (lane == 0 && m) b = atomicAdd(&cnt, __popc(m));
-      b = __shfl_sync(0xffffffffu, b, 0);
-      if (mine) queue[b + __popc(m & ((1u << lane) - 1u))] = j;
+      for (int q = 0; q < 16; q++)
+        if (fix_mine<kPolish>((words[q >> 2] >> (8 * (q & 3))) & 0xffu)) mask |= 1u << q;
+    } else {
+      for (int q = 0; q < 16; q++)
+        if (r0 + q < n && fix_mine<kPolish>(status[r0 + q])) mask |= 1u << q;
+    }
+    // warp-inclusive scan of the per-thread counts, one shared atomic per warp
+    const int mine = __popc(mask);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int base = 0;
+    if (lane == 31 && incl) base = atomicAdd(&cnt, incl);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - mine;
+    while (mask) {
+      const int q = __ffs(mask) - 1;
+      mask &= mask - 1;
+      queue[base++] = r0 + q;
     }
     __syncthreads();
     const int c = cnt;
@@ -627,10 +652,11 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   int rc = check_launch("eig3_fast_kernel");
   if (rc != SD_OK) return rc;
   const unsigned g2 = (unsigned)fixup_grid(n);
-  eig3_fixup_kernel<T, true><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
+  const int vec = aligned(status, 16) ? 1 : 0;
+  eig3_fixup_kernel<T, true><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status, vec);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;
-  eig3_fixup_kernel<T, false><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status);
+  eig3_fixup_kernel<T, false><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status, vec);
   return check_launch("eig3_literal_kernel");
 }
 
