@@ -77,10 +77,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # wait for the first sample so the timed region is covered
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.lines.clear()
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -377,7 +381,10 @@ def main():
                 "bound": "fp64", "achieved": fp64_achieved, "peak": fp64,
                 "unit": "TFLOP/s", "frac": fp64_achieved / fp64,
                 "traffic": ncu_traffic(cfg),
-                "kernel": "eig3_kernel<double>" if cost["metric_dim"] == 3 else "eig2_kernel",
+                "kernel": ("sd_eig3 call = eig3_fast_kernel + polish and literal fix-up "
+                           "kernels (the fast kernel is ~98% of the step, profiles/)")
+                if cost["metric_dim"] == 3 else "eig2_kernel",
+                "timing": "CUDA events around each sd_eig3 call on its stream; median",
                 "work_per_matrix": f"{cost['W']} FP64 instr-eq (BASELINE.md §4 cost model)",
                 "peak_source": "measured: sd_probe_dfma DFMA-chain microbenchmark, this run",
             },
