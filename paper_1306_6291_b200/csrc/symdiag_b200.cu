@@ -145,6 +145,9 @@ __global__ void __launch_bounds__(kThreads) eig3_kernel(const T* __restrict__ A,
 //   memory so the long fast path runs on dense warps (the degenerate-stress
 //   config is 1/3 generic, randomly interleaved).
 constexpr int kFastThreads = 256;
+#ifndef SD_FAST_MIN_BLOCKS
+#define SD_FAST_MIN_BLOCKS 4  // 64 registers: 32 warps/SM (3 blocks at 80 regs was 14% slower, profiles/r1_variants2.jsonl)
+#endif
 
 template <typename T>
 __device__ __forceinline__ sd::Sym3 load_row(const T* p) {
@@ -159,7 +162,7 @@ __device__ __forceinline__ sd::Sym3 load_row(const T* p) {
 }
 
 template <typename T, bool kVec>
-__global__ void __launch_bounds__(kFastThreads) eig3_fast_kernel(const T* __restrict__ A,
+__global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS) eig3_fast_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
                                                                  uint8_t* __restrict__ status) {

@@ -28,6 +28,8 @@ VARIANTS = {
     "eig_identity": {"SD_FAST_EIG_IDENTITY": 1},
     "div_rcp": {"SD_FAST_DIV_RCP": 1},
     "phi1_literal": {"SD_FAST_PHI1_LITERAL": 1},
+    "minblocks4": {"SD_FAST_MIN_BLOCKS": 4},
+    "minblocks5": {"SD_FAST_MIN_BLOCKS": 5},
 }
 
 
