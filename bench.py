@@ -179,7 +179,7 @@ def run_e2e(sd, config, n, steps, warmup, dev_index):
     lam = torch.empty((n, ow), dtype=dtype, pin_memory=True)
     ang = torch.empty((n,) if dim == 2 else (n, 3), dtype=dtype, pin_memory=True)
     st = torch.empty((n,), dtype=torch.uint8, pin_memory=True)
-    plan = sd.HostPlan(dev_index, chunk=1 << 21)
+    plan = sd.HostPlan(dev_index, chunk=1 << 20)  # best of a 2^17..2^22 sweep (tools/exp_e2e.py)
     call = (lambda: plan.eig2(A, lam, ang, st)) if dim == 2 else \
         (lambda: plan.eig3(A, lam, ang, st))
     for _ in range(warmup):
@@ -325,13 +325,17 @@ def main():
     import paper_1306_6291_b200 as sd
     from paper_1306_6291_b200 import workloads
 
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
     sd._lib.require_cuda()
+    # one rank per GPU; modulo only matters when a test runs more ranks than GPUs
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
+        # Control plane only (barriers, max-over-ranks of a scalar time): the
+        # data path has no collective, so a CPU (gloo) group is enough and
+        # keeps the run independent of NCCL topology.
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo")
 
     cfg = args.config
     n = args.n or workloads.CONFIGS[cfg]["n"]
@@ -343,13 +347,13 @@ def main():
         torch.cuda.synchronize()
 
     barrier()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev.index) as clk:
         barrier()
         per, launches, out = run_hot(sd, A, args.steps, args.warmup, cfg)
         barrier()
     total_ms = sum(per)
     if dist is not None:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([total_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_step = total_ms / args.steps
@@ -401,10 +405,10 @@ def main():
     if not args.no_e2e:
         # e2e through the public host-buffer C-ABI path (every rank)
         barrier()
-        times, h2d, d2h = run_e2e(sd, cfg, n, max(2, args.steps // 5), 1, local)
+        times, h2d, d2h = run_e2e(sd, cfg, n, max(2, args.steps // 5), 1, dev.index)
         tmax = statistics.median(times)
         if dist is not None:
-            t = torch.tensor([tmax], device=dev, dtype=torch.float64)
+            t = torch.tensor([tmax], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tmax = float(t.item())
         if result is not None:

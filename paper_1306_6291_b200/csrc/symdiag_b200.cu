@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(kThreads) eig3_kernel(const T* __restrict__ A,
 // Phase B: Generic rows of the whole block are compacted through shared
 //   memory so the long fast path runs on dense warps (the degenerate-stress
 //   config is 1/3 generic, randomly interleaved).
-constexpr int kFastThreads = 256;
+#ifndef SD_FAST_THREADS
+#define SD_FAST_THREADS 256
+#endif
+constexpr int kFastThreads = SD_FAST_THREADS;
 #ifndef SD_FAST_MIN_BLOCKS
 #define SD_FAST_MIN_BLOCKS 4  // 64 registers: 32 warps/SM (3 blocks at 80 regs was 14% slower, profiles/r1_variants2.jsonl)
 #endif
@@ -278,6 +281,9 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS) eig3_fast_ke
 // one-row blocks, no global workspace.  Two separate launches keep each
 // kernel's code small (the literal solver is ~13k SASS instructions).
 constexpr int kFixTile = 2048;
+#ifndef SD_FIX_MIN_BLOCKS
+#define SD_FIX_MIN_BLOCKS 4
+#endif
 constexpr int kFixThreads = 128;
 constexpr int kFixQueue = kFixTile + kFixThreads;
 
@@ -330,7 +336,7 @@ __device__ __forceinline__ bool fix_mine(unsigned byte) {
 }
 
 template <typename T, bool kPolish>
-__global__ void __launch_bounds__(kFixThreads) eig3_fixup_kernel(const T* __restrict__ A,
+__global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
                                                                  uint8_t* __restrict__ status,
@@ -391,7 +397,7 @@ int fixup_grid(int64_t n) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (nsm <= 0) nsm = 148;
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
-  const int64_t g = (int64_t)nsm * 4;
+  const int64_t g = (int64_t)nsm * SD_FIX_MIN_BLOCKS;
   return (int)(ntiles < g ? ntiles : g);
 }
 

@@ -25,11 +25,9 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "eig_identity": {"SD_FAST_EIG_IDENTITY": 1},
-    "div_rcp": {"SD_FAST_DIV_RCP": 1},
-    "phi1_literal": {"SD_FAST_PHI1_LITERAL": 1},
-    "minblocks4": {"SD_FAST_MIN_BLOCKS": 4},
-    "minblocks5": {"SD_FAST_MIN_BLOCKS": 5},
+    "fix6": {"SD_FIX_MIN_BLOCKS": 6},
+    "fix8": {"SD_FIX_MIN_BLOCKS": 8},
+    "fast128x8": {"SD_FAST_THREADS": 128, "SD_FAST_MIN_BLOCKS": 8},
 }
 
 
