@@ -21,13 +21,25 @@ __device__ __forceinline__ uint8_t diagonalize2(double a11, double a12, double a
   const double t = a11 + a22;
   const double sg = (dd < 0.0) ? -1.0 : 1.0;
   const double r = sg * py_hypot(dd, 2.0 * a12);
-  // SymMat2.scale (core.py:68-73)
-  const double scale =
-      pmax(1.0, py_sqrt(e, pow2(e, a11) + pow2(e, a22) + 2.0 * pow2(e, a12)));
-  const double eps = DEGENERACY_EPS_2 * scale;
+  // SymMat2.scale (core.py:68-73) gates the phi = 0 special case only
+  // (eig2.py:37-39): eps = 1e-14 max(1, ||A||_F).  Its sqrt is needed only
+  // when both |a11 - a22| and |a12| could be below eps, i.e. below
+  // 1e-14 * sqrt(F) * (1 + 2^-40) — otherwise the gate is decided without it.
+  const double fro2 = pow2(e, a11) + pow2(e, a22) + 2.0 * pow2(e, a12);
+  const double m = pmax(fabs(dd), fabs(a12));
+  bool zero_angle = false;
+  if (m * m <= 1.0000000001e-28 * pmax(1.0, fro2) || m <= DEGENERACY_EPS_2) {
+    const double eps = DEGENERACY_EPS_2 * pmax(1.0, py_sqrt(e, fro2));
+    zero_angle = fabs(dd) <= eps && fabs(a12) <= eps;
+  }
   double ph = 0.0;
-  if (!(fabs(dd) <= eps && fabs(a12) <= eps))
-    ph = wrap_half_pi(e, 0.5 * atan2(2.0 * a12 * sg, dd * sg));
+  if (!zero_angle) {
+    // wrap_half_pi of a value already in [-pi/2, pi/2]: remainder(x, pi) == x
+    // exactly there, so only the -pi/2 -> pi/2 and -0 -> +0 rules remain
+    ph = 0.5 * atan2(2.0 * a12 * sg, dd * sg);
+    if (ph <= -0.5 * kPi) ph = 0.5 * kPi;
+    if (ph == 0.0) ph = 0.0;
+  }
   if (e.code) {
     l1 = l2 = phi = qnan();
     return (uint8_t)e.code;

@@ -164,17 +164,26 @@ __device__ __forceinline__ sd::Sym3 load_row(const T* p) {
   return a;
 }
 
+// Rows per thread in phase A (the block classifies kFastRows * 256 rows,
+// then works through one queue of kFastRows * 256 slots).  More rows per
+// block lets the mixed config pack Generic and DoubleRoot work onto every
+// warp instead of leaving warps idle behind the block's slowest warp.
+#ifndef SD_FAST_ROWS
+#define SD_FAST_ROWS 1
+#endif
+constexpr int kFastRows = SD_FAST_ROWS;
+constexpr int kFastSlots = kFastRows * kFastThreads;
+
 template <typename T, bool kVec>
-__global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS) eig3_fast_kernel(const T* __restrict__ A,
-                                                                 int64_t n, T* __restrict__ lam,
-                                                                 T* __restrict__ ang,
-                                                                 uint8_t* __restrict__ status) {
+__global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
+    eig3_fast_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
+                     T* __restrict__ ang, uint8_t* __restrict__ status) {
   constexpr int W = kFastThreads / 32;
+  constexpr bool kStoreA = kFastRows == 1;  // else phase B reloads the row (L2 hit)
   __shared__ __align__(16) T stage[W][32 * 6];
-  __shared__ double qa[6][kFastThreads];
-  __shared__ double ql[3][kFastThreads];
-  __shared__ double qs[kFastThreads];
-  __shared__ int qrow[kFastThreads];
+  __shared__ double qa[kStoreA ? 6 : 1][kStoreA ? kFastSlots : 1];
+  __shared__ double ql[3][kFastSlots];
+  __shared__ int qrow[kFastSlots];
   __shared__ int qgen, qdbl;  // generic rows fill the queue from the front, double roots from the back
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -182,89 +191,98 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS) eig3_fast_ke
     qdbl = 0;
   }
   __syncthreads();
-  const int64_t row0 = ((int64_t)blockIdx.x * W + warp) * 32;
-  int cls = 2, reason = 0;
-  sd::Sym3 a;
-  double l[3], scale = 1.0;
-  int64_t i = row0 + lane;
-  if (row0 < n) {
-    const int rows = warp_stage<T, 6, kVec>(A, n, row0, stage[warp]);
-    if (lane < rows) {
-      const T* p = stage[warp] + 6 * lane;
-      a.a11 = (double)p[0];
-      a.a12 = (double)p[1];
-      a.a13 = (double)p[2];
-      a.a22 = (double)p[3];
-      a.a23 = (double)p[4];
-      a.a33 = (double)p[5];
-      cls = sd::classify3(a, l, scale, reason);
-      if (cls == 1 || cls == 4) {
+  const int64_t blk0 = (int64_t)blockIdx.x * kFastSlots;
+#pragma unroll 1
+  for (int rr = 0; rr < kFastRows; rr++) {
+    const int64_t row0 = blk0 + ((int64_t)rr * W + warp) * 32;
+    int cls = 2, reason = 0;
+    sd::Sym3 a;
+    double l[3], scale = 1.0;
+    const int64_t i = row0 + lane;
+    if (row0 < n) {
+      const int rows = warp_stage<T, 6, kVec>(A, n, row0, stage[warp]);
+      if (lane < rows) {
+        a = load_row(stage[warp] + 6 * lane);
+        cls = sd::classify3(a, l, scale, reason);
+        if (cls == 1 || cls == 4) {
 #pragma unroll
-        for (int k = 0; k < 3; k++) {
-          lam[3 * i + k] = (T)l[k];
-          ang[3 * i + k] = (T)0.0;
+          for (int k = 0; k < 3; k++) {
+            lam[3 * i + k] = (T)l[k];
+            ang[3 * i + k] = (T)0.0;
+          }
+          // fp32 outputs cannot carry the closed form into the polish: literal
+          status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT
+                                 : (sizeof(T) == 8 ? sd::kPolishTriple : sd::kDeferred);
+        } else if (cls == 2) {
+          status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
         }
-        // fp32 outputs cannot carry the closed form into the polish: literal
-        status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT
-                               : (sizeof(T) == 8 ? sd::kPolishTriple : sd::kDeferred);
-      } else if (cls == 2) {
-        status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
       }
+      __syncwarp();
     }
-  }
-  // warp-aggregated push into the block queue: generic rows at the front,
-  // double roots at the back, so phase-B warps are (almost) homogeneous
-  const unsigned mg = __ballot_sync(0xffffffffu, cls == 0);
-  const unsigned md = __ballot_sync(0xffffffffu, cls == 3);
-  int bg = 0, bd = 0;
-  if (lane == 0) {
-    if (mg) bg = atomicAdd(&qgen, __popc(mg));
-    if (md) bd = atomicAdd(&qdbl, __popc(md));
-  }
-  bg = __shfl_sync(0xffffffffu, bg, 0);
-  bd = __shfl_sync(0xffffffffu, bd, 0);
-  const unsigned below = (1u << lane) - 1u;
-  if (cls == 0 || cls == 3) {
-    const int slot = (cls == 0) ? bg + __popc(mg & below)
-                                : kFastThreads - 1 - (bd + __popc(md & below));
-    qa[0][slot] = a.a11;
-    qa[1][slot] = a.a12;
-    qa[2][slot] = a.a13;
-    qa[3][slot] = a.a22;
-    qa[4][slot] = a.a23;
-    qa[5][slot] = a.a33;
-    ql[0][slot] = l[0];
-    ql[1][slot] = l[1];
-    ql[2][slot] = l[2];
-    qs[slot] = scale;
-    qrow[slot] = (int)(i - (int64_t)blockIdx.x * kFastThreads);
+    // warp-aggregated push into the block queue: generic rows at the front,
+    // double roots at the back, so phase-B warps are (almost) homogeneous
+    const unsigned mg = __ballot_sync(0xffffffffu, cls == 0);
+    const unsigned md = __ballot_sync(0xffffffffu, cls == 3);
+    int bg = 0, bd = 0;
+    if (lane == 0) {
+      if (mg) bg = atomicAdd(&qgen, __popc(mg));
+      if (md) bd = atomicAdd(&qdbl, __popc(md));
+    }
+    bg = __shfl_sync(0xffffffffu, bg, 0);
+    bd = __shfl_sync(0xffffffffu, bd, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (cls == 0 || cls == 3) {
+      const int slot = (cls == 0) ? bg + __popc(mg & below)
+                                  : kFastSlots - 1 - (bd + __popc(md & below));
+      if (kStoreA) {
+        qa[0][slot] = a.a11;
+        qa[1][slot] = a.a12;
+        qa[2][slot] = a.a13;
+        qa[3][slot] = a.a22;
+        qa[4][slot] = a.a23;
+        qa[5][slot] = a.a33;
+      }
+      ql[0][slot] = l[0];
+      ql[1][slot] = l[1];
+      ql[2][slot] = l[2];
+      qrow[slot] = (int)(i - blk0);
+    }
   }
   __syncthreads();
-  const bool is_gen = tid < qgen;
-  if (!is_gen && tid < kFastThreads - qdbl) return;
-  sd::Sym3 g;
-  g.a11 = qa[0][tid];
-  g.a12 = qa[1][tid];
-  g.a13 = qa[2][tid];
-  g.a22 = qa[3][tid];
-  g.a23 = qa[4][tid];
-  g.a33 = qa[5][tid];
-  double gl[3] = {ql[0][tid], ql[1][tid], ql[2][tid]};
-  const int64_t r = (int64_t)blockIdx.x * kFastThreads + qrow[tid];
-  double phi[3];
-  uint8_t st = 0;
-  const int rc = is_gen ? sd::fast_generic(g, qs[tid], gl, phi, st)
-                        : sd::fast_double(g, qs[tid], gl, phi, st);
-  if (rc == sd::kFastDone || (rc == sd::kFastPolish && sizeof(T) == 8)) {
-    // done, or (fp64) closed form written with the polish pending
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      lam[3 * r + k] = (T)gl[k];
-      ang[3 * r + k] = (T)phi[k];
+  const int ng = qgen, nd = qdbl;
+#pragma unroll 1
+  for (int slot = tid; slot < kFastSlots; slot += kFastThreads) {
+    const bool is_gen = slot < ng;
+    if (!is_gen && slot < kFastSlots - nd) continue;
+    const int64_t r = blk0 + qrow[slot];
+    sd::Sym3 g;
+    if (kStoreA) {
+      g.a11 = qa[0][slot];
+      g.a12 = qa[1][slot];
+      g.a13 = qa[2][slot];
+      g.a22 = qa[3][slot];
+      g.a23 = qa[4][slot];
+      g.a33 = qa[5][slot];
+    } else {
+      g = load_row(A + 6 * r);
     }
-    status[r] = st;
-  } else {
-    status[r] = (rc == sd::kFastPolish) ? (uint8_t)(sd::kDeferred | (11 << 4)) : st;
+    double gl[3] = {ql[0][slot], ql[1][slot], ql[2][slot]};
+    double phi[3];
+    uint8_t st = 0;
+    const double scale = sd::fast_scale(g);
+    const int rc = is_gen ? sd::fast_generic(g, scale, gl, phi, st)
+                          : sd::fast_double(g, scale, gl, phi, st);
+    if (rc == sd::kFastDone || (rc == sd::kFastPolish && sizeof(T) == 8)) {
+      // done, or (fp64) closed form written with the polish pending
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        lam[3 * r + k] = (T)gl[k];
+        ang[3 * r + k] = (T)phi[k];
+      }
+      status[r] = st;
+    } else {
+      status[r] = (rc == sd::kFastPolish) ? (uint8_t)(sd::kDeferred | (11 << 4)) : st;
+    }
   }
 }
 
@@ -653,7 +671,7 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   if (n < 0 || (n > 0 && (!A || !lam || !ang || !status)))
     return set_err(SD_EINVAL, "sd_eig3: bad argument");
   if (n == 0) return SD_OK;
-  const unsigned g1 = (unsigned)((n + kFastThreads - 1) / kFastThreads);
+  const unsigned g1 = (unsigned)((n + kFastSlots - 1) / kFastSlots);
   if (aligned(A, 2 * sizeof(T)))
     eig3_fast_kernel<T, true><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
   else
@@ -714,7 +732,7 @@ int sd_eig3_classify_f64(const double* A, int64_t n, double* lam, double* ang, u
   if (n < 0 || (n > 0 && (!A || !lam || !ang || !status)))
     return set_err(SD_EINVAL, "sd_eig3_classify_f64: bad argument");
   if (n == 0) return SD_OK;
-  const unsigned g1 = (unsigned)((n + kFastThreads - 1) / kFastThreads);
+  const unsigned g1 = (unsigned)((n + kFastSlots - 1) / kFastSlots);
   if (aligned(A, 16))
     eig3_fast_kernel<double, true><<<g1, kFastThreads, 0, S(stream)>>>(A, n, lam, ang, status);
   else

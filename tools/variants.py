@@ -25,9 +25,8 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "fix6": {"SD_FIX_MIN_BLOCKS": 6},
-    "fix8": {"SD_FIX_MIN_BLOCKS": 8},
-    "fast128x8": {"SD_FAST_THREADS": 128, "SD_FAST_MIN_BLOCKS": 8},
+    "rows2": {"SD_FAST_ROWS": 2},
+    "rows4": {"SD_FAST_ROWS": 4},
 }
 
 
