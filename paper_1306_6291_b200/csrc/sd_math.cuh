@@ -100,7 +100,11 @@ __device__ __forceinline__ void py_sincos(Err& e, double x, double* s, double* c
 // math.hypot for two arguments: CPython 3.12 vector_norm (lossless scaling
 // by a power of two, error-free squares and compensated sums, one sqrt and
 // a differential correction).  Bit-identical to CPython given IEEE sqrt/fma.
-__device__ __forceinline__ double hypot_scaled(double a, double b, double scale) {
+// `scale` = 2^-e.  With kMul the final h / scale is evaluated as h * inv,
+// inv = 2^e, the same correctly rounded value (both are the exact h * 2^e
+// rounded once) — valid whenever 2^e is a finite double.
+template <bool kMul>
+__device__ __forceinline__ double hypot_scaled(double a, double b, double scale, double inv) {
   double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
   double v0 = __dmul_rn(a, scale), v1 = __dmul_rn(b, scale);
   {
@@ -125,7 +129,7 @@ __device__ __forceinline__ double hypot_scaled(double a, double b, double scale)
   frac2 += r;
   double t = csum - 1.0 + (frac1 + frac2);
   h += t / (2.0 * h);
-  return h / scale;
+  return kMul ? h * inv : h / scale;
 }
 
 // zero / inf / NaN / huge / subnormal magnitudes (CPython's special cases)
@@ -144,9 +148,9 @@ __device__ __noinline__ double py_hypot_abs_slow(double a, double b) {
     a = a / dmin;
     b = b / dmin;
     frexp(pmax(a, b), &ex);
-    return dmin * hypot_scaled(a, b, ldexp(1.0, -ex));
+    return dmin * hypot_scaled<false>(a, b, ldexp(1.0, -ex), 0.0);
   }
-  return hypot_scaled(a, b, ldexp(1.0, -ex));
+  return hypot_scaled<false>(a, b, ldexp(1.0, -ex), 0.0);
 }
 
 __device__ __forceinline__ double py_hypot(double x, double y) {
@@ -157,7 +161,8 @@ __device__ __forceinline__ double py_hypot(double x, double y) {
     return py_hypot_abs_slow(a, b);
   int ex = (int)((__double_as_longlong(mx) >> 52) & 0x7ff) - 1022;  // frexp exponent
   double scale = __longlong_as_double((long long)(1023 - ex) << 52);  // ldexp(1, -ex)
-  return hypot_scaled(a, b, scale);
+  const double inv = __longlong_as_double((long long)(1023 + ex) << 52);  // 2^ex
+  return hypot_scaled<true>(a, b, scale, inv);
 }
 
 // math.remainder(x, pi) (exact) and the wrap helpers of core.py:29-51
