@@ -25,8 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "rows2": {"SD_FAST_ROWS": 2},
-    "rows4": {"SD_FAST_ROWS": 4},
+    "noinline_math": {"SD_FAST_NOINLINE_MATH": 1},
 }
 
 
