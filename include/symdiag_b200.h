@@ -151,6 +151,29 @@ int sd_g_vectors_f64(const double* in, int64_t n, double* g, void* cuda_stream);
 int sd_compose_rotation_f64(const double* ang, int64_t n, double* d,
                             void* cuda_stream);
 
+/* ---- independent referees (SURVEY §8f "next" rows) ---------------------- */
+
+/* jacobi_eigen (oracle.py:45-84): cyclic-by-row Jacobi on packed rows of
+ * dimension dim (2: (a11,a12,a22); 3: six values) until the off-diagonal
+ * mass is <= tol^2 max(1, ||A||_F^2).  evals[n][dim] (final diagonal),
+ * evecs[n][dim*dim] row-major (columns are eigenvectors), sweeps[n],
+ * offdiag[n] (sqrt of the final off-diagonal sum of squares).
+ * status: 0, 1 = NoConvergence (oracle.py:63-64, > 100 sweeps),
+ * SD_ERR_NONFINITE_INPUT.                                                  */
+int sd_jacobi_f64(int dim, const double* A, int64_t n, double tol, double* evals,
+                  double* evecs, int32_t* sweeps, double* offdiag, uint8_t* status,
+                  void* cuda_stream);
+/* residuals (oracle.py:144-161) of a decomposition (lam[n][dim], d[n][dim*dim]
+ * row-major): out[n][dim+2] = (recon_rel, ortho, eigvec_res[0..dim-1]).    */
+int sd_residuals_f64(int dim, const double* A, const double* lam, const double* d,
+                     int64_t n, double* out, void* cuda_stream);
+
+/* cubic_roots_reference (oracle.py:87-133): bcd[n][3] = (b, c, d) of
+ * l^3 - b l^2 + c l + d -> roots[n][3] (ascending brackets, repeated roots
+ * as the reference orders them); status 0 or 1 = ComplexRootsDetected.    */
+int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots,
+                       uint8_t* status, void* cuda_stream);
+
 /* ---- host-buffer path (end-to-end: H2D, kernel, D2H, pipelined) ---------- */
 typedef struct sd_plan sd_plan;
 /* A plan owns device staging buffers for `chunk` matrices (double-buffered)

@@ -52,6 +52,9 @@ def lib():
         L.sdo_degenerate_double.argtypes = [P, P, I64, P, P, P]
         L.sdo_g_vectors.argtypes = [P, I64, P]
         L.sdo_compose_rotation.argtypes = [P, I64, P]
+        L.sdo_jacobi.argtypes = [ctypes.c_int, P, I64, ctypes.c_double, P, P, P, P, P,
+                                 ctypes.c_int]
+        L.sdo_residuals.argtypes = [ctypes.c_int, P, P, P, I64, P]
         L.sdo_py_hypot.argtypes = [ctypes.c_double, ctypes.c_double]
         L.sdo_py_hypot.restype = ctypes.c_double
         _lib = L
@@ -181,6 +184,29 @@ def compose_rotation(ang):
     ang = _c(ang, width=3)
     out = np.empty((ang.shape[0], 9))
     lib().sdo_compose_rotation(_p(ang), ang.shape[0], _p(out))
+    return out
+
+
+def jacobi(A, dim: int = 3, tol: float = 1e-13, nthreads: int = 1):
+    """jacobi_eigen (oracle.py:45-84) over packed rows -> dict(evals, evecs
+    [n, dim*dim] row-major, sweeps, offdiag, status (0, 1 NoConvergence, 8))."""
+    w = 3 if dim == 2 else 6
+    A = _c(A, width=w)
+    n = A.shape[0]
+    out = dict(evals=np.empty((n, dim)), evecs=np.empty((n, dim * dim)),
+               sweeps=np.empty(n, np.int32), offdiag=np.empty(n), status=np.empty(n, np.uint8))
+    lib().sdo_jacobi(dim, _p(A), n, tol, _p(out["evals"]), _p(out["evecs"]), _p(out["sweeps"]),
+                     _p(out["offdiag"]), _p(out["status"]), nthreads)
+    return out
+
+
+def residuals(A, lam, d, dim: int = 3):
+    """residuals (oracle.py:144-161) -> [n, dim + 2] = (recon_rel, ortho,
+    eigvec_res...)."""
+    w = 3 if dim == 2 else 6
+    A, lam, d = _c(A, width=w), _c(lam, width=dim), _c(d, width=dim * dim)
+    out = np.empty((A.shape[0], dim + 2))
+    lib().sdo_residuals(dim, _p(A), _p(lam), _p(d), A.shape[0], _p(out))
     return out
 
 

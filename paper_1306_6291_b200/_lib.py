@@ -35,6 +35,9 @@ SIGNATURES = {
     "sd_f_vectors_f64": [_P, _I64, _P, _P],
     "sd_g_vectors_f64": [_P, _I64, _P, _P],
     "sd_compose_rotation_f64": [_P, _I64, _P, _P],
+    "sd_jacobi_f64": [_I, _P, _I64, ctypes.c_double, _P, _P, _P, _P, _P, _P],
+    "sd_residuals_f64": [_I, _P, _P, _P, _I64, _P, _P],
+    "sd_cubic_roots_f64": [_P, _I64, _P, _P, _P],
     "sd_plan_create": [_I, _I64, ctypes.POINTER(_P)],
     "sd_plan_destroy": [_P],
     "sd_eig3_f64_host": [_P, _P, _I64, _P, _P, _P],

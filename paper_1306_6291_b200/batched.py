@@ -241,6 +241,58 @@ def compose_rotation_batched(ang):
     return d
 
 
+class JacobiBatch(NamedTuple):
+    evals: torch.Tensor      # [n, dim] final diagonal (Jacobi order, unsorted)
+    evecs: torch.Tensor      # [n, dim, dim] columns are eigenvectors
+    sweeps: torch.Tensor     # [n] int32
+    offdiag: torch.Tensor    # [n]
+    status: torch.Tensor     # [n] uint8: 0, 1 NoConvergence, 8 NonFiniteInput
+
+
+def jacobi_batched(A: torch.Tensor, dim: int = 3, tol: float = 1e-13) -> JacobiBatch:
+    """Batched jacobi_eigen (oracle.py:45-84), an independent referee."""
+    if tol <= 0.0:
+        raise ValueError("tol must be positive")
+    A = _check_input(A, 3 if dim == 2 else 6)
+    n, dev = A.shape[0], A.device
+    ev = _empty(n, dim, dev)
+    vec = _empty(n, dim * dim, dev)
+    sw = torch.empty((n,), dtype=torch.int32, device=dev)
+    od = _empty(n, 0, dev)
+    st = _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_jacobi_f64", dim, A.data_ptr(), n, float(tol), ev.data_ptr(),
+                  vec.data_ptr(), sw.data_ptr(), od.data_ptr(), st.data_ptr(), _stream())
+    return JacobiBatch(ev, vec.view(n, dim, dim), sw, od, st)
+
+
+def residuals_batched(A: torch.Tensor, lam: torch.Tensor, d: torch.Tensor,
+                      dim: int = 3) -> torch.Tensor:
+    """Batched residuals (oracle.py:144-161): [n, dim+2] = (recon_rel, ortho,
+    eigvec_res...) for decompositions (lam [n,dim], d [n,dim,dim])."""
+    A = _check_input(A, 3 if dim == 2 else 6)
+    lam = _check_input(lam.reshape(-1, dim), dim)
+    d = _check_input(d.reshape(-1, dim * dim), dim * dim)
+    n, dev = A.shape[0], A.device
+    out = _empty(n, dim + 2, dev)
+    with torch.cuda.device(dev):
+        _lib.call("sd_residuals_f64", dim, A.data_ptr(), lam.data_ptr(), d.data_ptr(), n,
+                  out.data_ptr(), _stream())
+    return out
+
+
+def cubic_roots_batched(bcd: torch.Tensor):
+    """Batched cubic_roots_reference (oracle.py:87-133): roots [n,3] and
+    status [n] (0, or 1 = ComplexRootsDetected)."""
+    bcd = _check_input(bcd, 3)
+    n, dev = bcd.shape[0], bcd.device
+    roots, st = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8)
+    with torch.cuda.device(dev):
+        _lib.call("sd_cubic_roots_f64", bcd.data_ptr(), n, roots.data_ptr(), st.data_ptr(),
+                  _stream())
+    return roots, st
+
+
 class HostPlan:
     """End-to-end path over HOST buffers (numpy or pinned torch CPU tensors):
     chunked H2D -> kernel -> D2H, pipelined over three streams in C++

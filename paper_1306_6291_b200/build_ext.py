@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libsymdiag_b200.so"
 SOURCES = ["symdiag_b200.cu", "sd_host.cu"]
-HEADERS = ["sd_math.cuh", "sd_eig3.cuh", "sd_eig2.cuh"]
+HEADERS = ["sd_math.cuh", "sd_eig3.cuh", "sd_eig2.cuh", "sd_fast3.cuh", "sd_jacobi.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

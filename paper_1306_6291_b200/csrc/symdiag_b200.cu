@@ -20,6 +20,7 @@
 #include "sd_eig2.cuh"
 #include "sd_eig3.cuh"
 #include "sd_fast3.cuh"
+#include "sd_jacobi.cuh"
 
 namespace {
 
@@ -649,6 +650,86 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(int iters, double* sink
   sink[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// ---- referees: batched Jacobi and residuals (sd_jacobi.cuh) ----------------
+template <int N>
+__device__ __forceinline__ void load_full(const double* A, int64_t i, double* m, bool& finite) {
+  if (N == 2) {
+    const double a11 = A[3 * i], a12 = A[3 * i + 1], a22 = A[3 * i + 2];
+    m[0] = a11;
+    m[1] = a12;
+    m[2] = a12;
+    m[3] = a22;
+    finite = sd::is_finite(a11) && sd::is_finite(a12) && sd::is_finite(a22);
+  } else {
+    const sd::Sym3 a = sd::unpack3(A + 6 * i);
+    m[0] = a.a11, m[1] = a.a12, m[2] = a.a13;
+    m[3] = a.a12, m[4] = a.a22, m[5] = a.a23;
+    m[6] = a.a13, m[7] = a.a23, m[8] = a.a33;
+    finite = sd::finite3(a);
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) jacobi_kernel(const double* A, int64_t n, double tol,
+                                                     double* evals, double* evecs,
+                                                     int32_t* sweeps, double* offdiag,
+                                                     uint8_t* status) {
+  const int64_t i = gtid();
+  if (i >= n) return;
+  double m[N * N], v[N * N];
+  bool finite;
+  load_full<N>(A, i, m, finite);
+  if (!finite) {  // SymMat2/3 construction raises NonFiniteInput (core.py:62, :90)
+#pragma unroll
+    for (int k = 0; k < N; k++) evals[N * i + k] = sd::qnan();
+#pragma unroll
+    for (int k = 0; k < N * N; k++) evecs[N * N * i + k] = sd::qnan();
+    sweeps[i] = 0;
+    offdiag[i] = sd::qnan();
+    status[i] = SD_ERR_NONFINITE_INPUT;
+    return;
+  }
+  int sw;
+  double od;
+  const int rc = sd::jacobi<N>(m, tol, v, sw, od);
+#pragma unroll
+  for (int k = 0; k < N; k++) evals[N * i + k] = m[N * k + k];
+#pragma unroll
+  for (int k = 0; k < N * N; k++) evecs[N * N * i + k] = v[k];
+  sweeps[i] = sw;
+  offdiag[i] = od;
+  status[i] = (uint8_t)rc;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) residuals_kernel(const double* A, const double* lam,
+                                                        const double* d, int64_t n,
+                                                        double* out) {
+  const int64_t i = gtid();
+  if (i >= n) return;
+  double m[N * N], l[N], dd[N * N], o[N + 2];
+  bool finite;
+  load_full<N>(A, i, m, finite);
+#pragma unroll
+  for (int k = 0; k < N; k++) l[k] = lam[N * i + k];
+#pragma unroll
+  for (int k = 0; k < N * N; k++) dd[k] = d[N * N * i + k];
+  sd::residuals<N>(m, l, dd, o);
+#pragma unroll
+  for (int k = 0; k < N + 2; k++) out[(N + 2) * i + k] = o[k];
+}
+
+__global__ void cubic_roots_kernel(const double* bcd, int64_t n, double* roots,
+                                   uint8_t* status) {
+  const int64_t i = gtid();
+  if (i >= n) return;
+  double r[3];
+  const int rc = sd::cubic_roots(bcd[3 * i], bcd[3 * i + 1], bcd[3 * i + 2], r);
+#pragma unroll
+  for (int k = 0; k < 3; k++) roots[3 * i + k] = rc ? sd::qnan() : r[k];
+  status[i] = (uint8_t)rc;
+}
+
 inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
 template <typename T, bool kReport>
@@ -792,6 +873,31 @@ int sd_g_vectors_f64(const double* in, int64_t n, double* g, void* stream) {
 }
 int sd_compose_rotation_f64(const double* ang, int64_t n, double* d, void* stream) {
   SIMPLE_LAUNCH(compose_rotation_kernel, ang, n, d);
+}
+
+int sd_jacobi_f64(int dim, const double* A, int64_t n, double tol, double* evals,
+                  double* evecs, int32_t* sweeps, double* offdiag, uint8_t* status,
+                  void* stream) {
+  if ((dim != 2 && dim != 3) || !(tol > 0.0))
+    return set_err(SD_EINVAL, "sd_jacobi_f64: dim must be 2 or 3 and tol positive");
+  if (dim == 2) {
+    SIMPLE_LAUNCH(jacobi_kernel<2>, A, n, tol, evals, evecs, sweeps, offdiag, status);
+  }
+  SIMPLE_LAUNCH(jacobi_kernel<3>, A, n, tol, evals, evecs, sweeps, offdiag, status);
+}
+
+int sd_residuals_f64(int dim, const double* A, const double* lam, const double* d, int64_t n,
+                     double* out, void* stream) {
+  if (dim != 2 && dim != 3) return set_err(SD_EINVAL, "sd_residuals_f64: dim must be 2 or 3");
+  if (dim == 2) {
+    SIMPLE_LAUNCH(residuals_kernel<2>, A, lam, d, n, out);
+  }
+  SIMPLE_LAUNCH(residuals_kernel<3>, A, lam, d, n, out);
+}
+
+int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots, uint8_t* status,
+                       void* stream) {
+  SIMPLE_LAUNCH(cubic_roots_kernel, bcd, n, roots, status);
 }
 
 int sd_probe_dfma(int blocks, int iters, double* sink, double* dfma_total, void* stream) {

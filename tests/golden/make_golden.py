@@ -68,6 +68,12 @@ def main():
         A = sets3[name]
         s = refrun.run_stages(A)
         save(f"stages_{name}", A=A, **s)
+    # oracle.py referees: Jacobi, cubic roots, residuals
+    ref3 = np.concatenate([cases.edge_cases_3x3(), workloads.generate("c2", 1024),
+                           workloads.generate("c3", 1024)])
+    save("referee3", A=ref3, **refrun.run_referees(ref3, 3))
+    ref2 = np.concatenate([cases.edge_cases_2x2(), workloads.generate("c1", 1024)])
+    save("referee2", A=ref2, **refrun.run_referees(ref2, 2))
 
 
 if __name__ == "__main__":

@@ -181,6 +181,61 @@ def run_eig2(A: np.ndarray, with_d: bool = False):
     return out
 
 
+def run_referees(A: np.ndarray, dim: int):
+    """oracle.py referees: jacobi_eigen per row, and for 3x3 also
+    cubic_roots_reference on char_coeffs and residuals of diagonalize3."""
+    symdiag, eig3, core = _import()
+    from symdiag import oracle as RO
+    w = 3 if dim == 2 else 6
+    A = np.asarray(A, dtype=np.float64).reshape(-1, w)
+    n = A.shape[0]
+    evals = np.full((n, dim), np.nan)
+    evecs = np.full((n, dim * dim), np.nan)
+    sweeps = np.zeros(n, np.int32)
+    offdiag = np.full(n, np.nan)
+    jstatus = np.zeros(n, np.uint8)
+    roots = np.full((n, 3), np.nan)
+    rstatus = np.zeros(n, np.uint8)
+    resid = np.full((n, dim + 2), np.nan)
+    for i in range(n):
+        try:
+            if dim == 2:
+                m = symdiag.SymMat2(a11=float(A[i, 0]), a22=float(A[i, 2]), a12=float(A[i, 1]))
+            else:
+                m = sym3_from_packed(symdiag, A[i])
+        except core.NonFiniteInput:
+            jstatus[i] = rstatus[i] = NONFINITE
+            continue
+        try:
+            r = RO.jacobi_eigen(m)
+            evals[i], evecs[i] = r.eigenvalues, r.eigenvectors.reshape(-1)
+            sweeps[i], offdiag[i] = r.sweeps, r.offdiag_final
+        except RO.NoConvergence:
+            jstatus[i] = 1
+        if dim == 3:
+            try:
+                roots[i] = RO.cubic_roots_reference(eig3.char_coeffs(m))
+            except RO.ComplexRootsDetected:
+                rstatus[i] = 1
+            except (OverflowError, ValueError):
+                rstatus[i] = 2
+            try:
+                dec = eig3.diagonalize3(m)
+                rr = RO.residuals(m, dec)
+                resid[i] = [rr[0], rr[1], *rr[2]]
+            except Exception:  # noqa: BLE001 — rows the solver rejects
+                pass
+        else:
+            try:
+                dec = symdiag.diagonalize2(m)
+                rr = RO.residuals(m, dec)
+                resid[i] = [rr[0], rr[1], *rr[2]]
+            except Exception:  # noqa: BLE001 — rows the solver rejects
+                pass
+    return dict(evals=evals, evecs=evecs, sweeps=sweeps, offdiag=offdiag, jstatus=jstatus,
+                roots=roots, rstatus=rstatus, resid=resid)
+
+
 def run_stages(A: np.ndarray):
     """Stage-level reference outputs: char_coeffs, compute_pq, eigenvalues3,
     pq_expanded, compute_v/compute_w (with exception codes)."""

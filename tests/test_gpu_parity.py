@@ -309,3 +309,78 @@ def test_full_size_properties_c2():
                         A[:, 2], A[:, 4], A[:, 5]], 1).view(-1, 3, 3)
     res = torch.linalg.matrix_norm(rec - full) / s
     assert float(res.max()) <= 1e-10
+
+
+# ---- referees: GPU Jacobi, residuals, cubic roots ------------
+@pytest.mark.parametrize("dim", [3, 2])
+def test_jacobi_matches_reference_golden(dim):
+    """Jacobi has no transcendental calls: with numpy's FMA orders, CPython's
+    hypot and IEEE division it is expected to match the reference bit for
+    bit; the only difference allowed is x*x for numpy's pow(x, 2) in the
+    convergence test (one sweep more or less, values then within 1e-15)."""
+    g = load_golden(f"referee{dim}")
+    r = sd.jacobi_batched(torch.as_tensor(g["A"]).to(DEV), dim=dim)
+    torch.cuda.synchronize()
+    st = r.status.cpu().numpy()
+    assert np.array_equal(st, g["jstatus"])
+    ok = st == 0
+    ev, vec = r.evals.cpu().numpy()[ok], r.evecs.cpu().numpy().reshape(len(st), -1)[ok]
+    same = np.all(ev == g["evals"][ok], axis=1) & np.all(vec == g["evecs"][ok], axis=1)
+    assert same.mean() >= 0.999, same.mean()
+    sc = np.maximum(1.0, np.abs(g["evals"][ok]).max(axis=1))
+    assert np.all(np.abs(ev - g["evals"][ok]).max(axis=1) <= 1e-15 * sc)
+
+
+def test_jacobi_large_matches_oracle():
+    A = workloads.generate("c2", 1 << 16)
+    ref = O.jacobi(A, dim=3, nthreads=O.default_threads())
+    r = sd.jacobi_batched(torch.as_tensor(A).to(DEV), dim=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.status.cpu().numpy(), ref["status"])
+    ev = r.evals.cpu().numpy()
+    exact = np.all(ev == ref["evals"], axis=1)
+    assert exact.mean() >= 0.999
+    assert np.abs(ev - ref["evals"]).max() <= 1e-13
+    assert np.mean(r.sweeps.cpu().numpy() == ref["sweeps"]) >= 0.999
+
+
+@pytest.mark.parametrize("dim", [3, 2])
+def test_residuals_match_reference_golden(dim):
+    g = load_golden(f"referee{dim}")
+    ok = ~np.isnan(g["resid"][:, 0])
+    A = g["A"][ok]
+    dec = O.eig3(A, d=True) if dim == 3 else O.eig2(A, d=True)
+    good = (dec["status"] & 0x80) == 0  # polished D is not pinned
+    out = sd.residuals_batched(torch.as_tensor(A).to(DEV), torch.as_tensor(dec["lam"]).to(DEV),
+                               torch.as_tensor(dec["d"]).to(DEV), dim=dim).cpu().numpy()
+    assert np.all(np.abs(out[good] - g["resid"][ok][good]) <= 1e-15)
+
+
+def test_cubic_roots_match_reference_golden():
+    g = load_golden("referee3")
+    bcd, st = O.char_coeffs(g["A"])
+    use = (st == 0) & (g["rstatus"] != 2)
+    roots, rst = sd.cubic_roots_batched(torch.as_tensor(bcd[use]).to(DEV))
+    rst = rst.cpu().numpy()
+    assert np.array_equal(rst, g["rstatus"][use])
+    okr = rst == 0
+    ref = g["roots"][use][okr]
+    got = roots.cpu().numpy()[okr]
+    sc = np.maximum(1.0, np.abs(ref).max(axis=1, keepdims=True))
+    # brentq (xtol 1e-15, rtol 4 eps) vs bisection to adjacent doubles
+    assert np.all(np.abs(got - ref) <= 1e-13 * sc)
+
+
+def test_referee_scalar_api():
+    a = sd.SymMat3(2.0, 1.0, 3.0, 0.5, -0.25, 0.125)
+    jr = sd.jacobi_eigen(a)
+    dec = sd.diagonalize3(a)
+    assert np.allclose(np.sort(jr.eigenvalues), np.sort(dec.lambdas), atol=1e-12)
+    recon, ortho, ev = sd.residuals(a, dec)
+    assert recon <= 1e-14 and ortho <= 1e-14 and max(ev) <= 1e-14
+    roots = sd.cubic_roots_reference(sd.char_coeffs(a))
+    assert np.allclose(sorted(roots), sorted(dec.lambdas), atol=1e-12)
+    with pytest.raises(ValueError):
+        sd.jacobi_eigen(a, tol=0.0)
+    r2 = sd.jacobi_eigen(sd.SymMat2(1.0, 0.0, 2.0))
+    assert np.allclose(np.sort(r2.eigenvalues), [-1.0, 2.0], atol=1e-13)
