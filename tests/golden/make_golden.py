@@ -23,6 +23,7 @@ Sets (prefixes of the benchmark configs are exact, see workloads.py):
 
 from __future__ import annotations
 
+import json
 import sys
 from pathlib import Path
 
@@ -74,6 +75,31 @@ def main():
     save("referee3", A=ref3, **refrun.run_referees(ref3, 3))
     ref2 = np.concatenate([cases.edge_cases_2x2(), workloads.generate("c1", 1024)])
     save("referee2", A=ref2, **refrun.run_referees(ref2, 2))
+    # JSON-lines front end: the reference's cmd_solve on a corpus built here
+    # (edge rows it accepts + malformed lines), expected output kept verbatim
+    import io
+    symdiag, eig3, core = refrun._import()
+    from symdiag import cli as RC
+    lines = []
+    r3 = refrun.run_eig3(sets3["edge"])
+    for i, row in enumerate(sets3["edge"]):
+        if (r3["status"][i] & 0x0F) < 8:
+            a11, a12, a13, a22, a23, a33 = (float(x) for x in row)
+            lines.append(json.dumps({"id": f"e3-{i}", "a11": a11, "a22": a22, "a33": a33,
+                                     "a12": a12, "a13": a13, "a23": a23}))
+    r2 = refrun.run_eig2(cases.edge_cases_2x2())
+    for i, row in enumerate(cases.edge_cases_2x2()):
+        if r2["status"][i] < 8:
+            lines.append(json.dumps({"id": f"e2-{i}", "a11": float(row[0]),
+                                     "a22": float(row[2]), "a12": float(row[1])}))
+    lines[3:3] = ['{"a11": 1, "a22": 2}', "not json", '{"id": 5, "a11": 1, "a22": 2, "a12": 0}',
+                  '{"a11": true, "a22": 2, "a12": 0}', "[1, 2, 3]", ""]
+    text = "\n".join(lines) + "\n"
+    out = io.StringIO()
+    rc = RC.cmd_solve(io.StringIO(text), out)
+    (HERE / "cli_solve_input.jsonl").write_text(text)
+    (HERE / "cli_solve_expected.jsonl").write_text(out.getvalue())
+    print("wrote cli_solve_{input,expected}.jsonl", len(lines), "lines, rc", rc)
 
 
 if __name__ == "__main__":

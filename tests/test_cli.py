@@ -1,0 +1,128 @@
+"""JSON-lines front end against the reference's own
+cmd_solve output on a corpus built by tests/golden/make_golden.py."""
+
+from __future__ import annotations
+
+import io
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1306_6291_b200 import cli
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def expected_lines():
+    return (GOLDEN / "cli_solve_expected.jsonl").read_text().splitlines()
+
+
+def test_parse_errors_match_reference_messages():
+    """Every malformed line gets the reference's inline error text."""
+    inp = (GOLDEN / "cli_solve_input.jsonl").read_text().splitlines()
+    exp = [json.loads(x) for x in expected_lines()]
+    errs = [e["error"] for e in exp if "error" in e]
+    got = []
+    for line in inp:
+        if not line.strip():
+            continue
+        try:
+            cli.parse_record(line)
+        except cli.ParseError as e:
+            got.append(str(e))
+    assert got == errs
+
+
+def test_dumps_formatting_matches_reference_style():
+    obj = {"id": "x", "dim": 3, "v": [1.0, 0.1, -0.0, 1e-300, 2.5e16], "b": None, "t": True,
+           "r": {"a": 1.0000000000000002}}
+    s = cli.dumps(obj)
+    assert s == ('{"id": "x", "dim": 3, "v": [1, 0.10000000000000001, -0, 1e-300, '
+                 '25000000000000000], "b": null, "t": true, "r": {"a": 1.0000000000000002}}')
+    refrun = pytest.importorskip("refrun")
+    if refrun.available():
+        refrun._import()
+        from symdiag import cli as RC
+        assert s == RC._dumps(obj)
+
+
+def test_random_stream_matches_reference_generator():
+    rows = cli.random_symmetric_rows(50, 42)
+    rng = np.random.default_rng(42)
+    for r in rows:
+        a11, a22, a33, a12, a13, a23 = rng.uniform(-1.0, 1.0, 6)
+        assert list(r) == [a11, a12, a13, a22, a23, a33]
+
+
+torch = pytest.importorskip("torch")
+gpu = pytest.mark.gpu
+
+
+def _solve(text, **kw):
+    out = io.StringIO()
+    rc = cli.cmd_solve(io.StringIO(text), out, **kw)
+    return rc, out.getvalue().splitlines()
+
+
+@gpu
+def test_cli_solve_matches_reference_output():
+    rc, got = _solve((GOLDEN / "cli_solve_input.jsonl").read_text())
+    exp = expected_lines()
+    assert rc == 0 and len(got) == len(exp)
+    identical = 0
+    for g_line, e_line in zip(got, exp):
+        identical += g_line == e_line
+        g, e = json.loads(g_line), json.loads(e_line)
+        if "error" in e:
+            assert g == e
+            continue
+        assert g["id"] == e["id"] and g["dim"] == e["dim"] and g["branch"] == e["branch"]
+        sc = max(1.0, max(abs(x) for x in e["eigenvalues"]))
+        assert max(abs(a - b) for a, b in zip(g["eigenvalues"], e["eigenvalues"])) <= 1e-12 * sc
+        assert g["eigenvalues_sorted"] == sorted(g["eigenvalues"], reverse=True)
+        assert g["euler_angles"] == g["angles"]
+        assert set(g["residuals"]) == set(e["residuals"])
+        if e["branch"] in ("Generic", "AlreadyDiagonal2D", None):
+            for a, b in zip(g["angles"], e["angles"]):
+                d = abs(math.remainder(a - b, math.pi))
+                edge = min(abs(b), abs(abs(b) - math.pi / 2)) < 1e-2
+                assert d <= (1e-7 if edge else 1e-10), (g["id"], a, b)
+            assert g["residuals"]["recon_rel"] <= max(4 * e["residuals"]["recon_rel"], 1e-12)
+    # byte-identical wherever the GPU's libm agrees with glibc to the last bit
+    assert identical >= len(exp) // 2, identical
+
+
+@gpu
+def test_cli_solver_exception_aborts_or_inlines():
+    text = ('{"id": "ok", "a11": 1, "a22": 2, "a33": 3, "a12": 0.1, "a13": 0.2, "a23": 0.3}\n'
+            '{"id": "big", "a11": 1e200, "a22": 2, "a33": 3, "a12": 0, "a13": 0, "a23": 0}\n')
+    with pytest.raises(OverflowError):
+        _solve(text)
+    rc, lines = _solve(text, inline_errors=True)
+    assert rc == 0 and json.loads(lines[1]) == {"id": "big",
+                                                "error": json.loads(lines[1])["error"]}
+    assert json.loads(lines[1])["error"].startswith("OverflowError")
+
+
+@gpu
+def test_cli_verify_and_corrupt_hook():
+    text = (GOLDEN / "cli_solve_input.jsonl").read_text()
+    good = "\n".join(x for x in text.splitlines() if x.startswith('{"id": "e'))
+    out = io.StringIO()
+    assert cli.cmd_verify(io.StringIO(good), out, 1e-6) == 0
+    s = json.loads(out.getvalue())
+    assert s["fail"] == 0 and s["records"] == len(good.splitlines())
+    out = io.StringIO()
+    assert cli.cmd_verify(io.StringIO(good), out, 1e-6, corrupt=True) == 1
+    assert json.loads(out.getvalue())["fail"] > 0
+
+
+@gpu
+def test_cli_bench_reports_ratio():
+    out = io.StringIO()
+    assert cli.cmd_bench(out, 100_000, 42) == 0
+    r = json.loads(out.getvalue())
+    assert r["n"] == 100_000 and r["throughput_ratio_closed_over_jacobi"] > 0

@@ -367,8 +367,18 @@ def test_cubic_roots_match_reference_golden():
     ref = g["roots"][use][okr]
     got = roots.cpu().numpy()[okr]
     sc = np.maximum(1.0, np.abs(ref).max(axis=1, keepdims=True))
-    # brentq (xtol 1e-15, rtol 4 eps) vs bisection to adjacent doubles
-    assert np.all(np.abs(got - ref) <= 1e-13 * sc)
+    # brentq (xtol 1e-15, rtol 4 eps) vs bisection to adjacent doubles: equal
+    # to 1e-13 where the root is well conditioned; near a multiple root the
+    # polynomial is flat inside its rounding noise and any point there is a
+    # root, so the GPU root must then be as good a root as the reference's
+    b, c, d = (bcd[use][okr][:, k:k + 1] for k in range(3))
+    poly = lambda x: ((x - b) * x + c) * x + d  # noqa: E731
+    noise = 8 * np.finfo(float).eps * (np.abs(got) ** 3 + np.abs(b) * got ** 2
+                                       + np.abs(c) * np.abs(got) + np.abs(d))
+    close = np.abs(got - ref) <= 1e-13 * sc
+    flat = np.abs(poly(got)) <= np.maximum(noise, np.abs(poly(ref)))
+    assert np.all(close | flat)
+    assert close.mean() >= 0.99
 
 
 def test_referee_scalar_api():
@@ -382,5 +392,6 @@ def test_referee_scalar_api():
     assert np.allclose(sorted(roots), sorted(dec.lambdas), atol=1e-12)
     with pytest.raises(ValueError):
         sd.jacobi_eigen(a, tol=0.0)
-    r2 = sd.jacobi_eigen(sd.SymMat2(1.0, 0.0, 2.0))
-    assert np.allclose(np.sort(r2.eigenvalues), [-1.0, 2.0], atol=1e-13)
+    r2 = sd.jacobi_eigen(sd.SymMat2(1.0, 0.0, 2.0))  # (a11, a22, a12): (1 +- sqrt 17) / 2
+    assert np.allclose(np.sort(r2.eigenvalues), [(1 - 17 ** 0.5) / 2, (1 + 17 ** 0.5) / 2],
+                       atol=1e-13)
