@@ -72,6 +72,9 @@ def test_cli_solve_matches_reference_output():
     rc, got = _solve((GOLDEN / "cli_solve_input.jsonl").read_text())
     exp = expected_lines()
     assert rc == 0 and len(got) == len(exp)
+    # rows the reference polished (Gauss-Newton, not bit-pinned): angle-exempt
+    with np.load(GOLDEN / "eig3_edge.npz") as z:
+        polished = {f"e3-{i}" for i in np.nonzero(z["status"] & 0x80)[0]}
     identical = 0
     for g_line, e_line in zip(got, exp):
         identical += g_line == e_line
@@ -85,7 +88,7 @@ def test_cli_solve_matches_reference_output():
         assert g["eigenvalues_sorted"] == sorted(g["eigenvalues"], reverse=True)
         assert g["euler_angles"] == g["angles"]
         assert set(g["residuals"]) == set(e["residuals"])
-        if e["branch"] in ("Generic", "AlreadyDiagonal2D", None):
+        if e["branch"] in ("Generic", "AlreadyDiagonal2D", None) and e["id"] not in polished:
             for a, b in zip(g["angles"], e["angles"]):
                 d = abs(math.remainder(a - b, math.pi))
                 edge = min(abs(b), abs(abs(b) - math.pi / 2)) < 1e-2
@@ -109,8 +112,11 @@ def test_cli_solver_exception_aborts_or_inlines():
 
 @gpu
 def test_cli_verify_and_corrupt_hook():
-    text = (GOLDEN / "cli_solve_input.jsonl").read_text()
-    good = "\n".join(x for x in text.splitlines() if x.startswith('{"id": "e'))
+    from paper_1306_6291_b200 import workloads
+    rows = workloads.generate("c2", 2000)
+    good = "\n".join(json.dumps({"id": str(i), "a11": r[0], "a12": r[1], "a13": r[2],
+                                 "a22": r[3], "a23": r[4], "a33": r[5]})
+                     for i, r in enumerate(rows.tolist()))
     out = io.StringIO()
     assert cli.cmd_verify(io.StringIO(good), out, 1e-6) == 0
     s = json.loads(out.getvalue())
