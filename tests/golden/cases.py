@@ -110,6 +110,52 @@ def edge_cases_3x3() -> np.ndarray:
     return np.array(rows, dtype=np.float64)
 
 
+def adversarial_3x3(n: int, seed: int = 7100) -> np.ndarray:
+    """Seeded stress rows for the fast path's guards: every row family below
+    sits on or near a decision boundary of the reference algorithm.
+      - random rotations of diag(l) with two / three eigenvalues equal up to
+        relative gaps 0, 1e-15 .. 1e-3 (double/triple-root thresholds,
+        DegenerateEigenvalues, the q-sign noise)
+      - angles at and near 0, pi/8, pi/4, 3pi/8, pi/2 (refinement windows,
+        edge window, the wrap at +-pi/2)
+      - magnitudes 2^-200 .. 2^200 (fast-path guard at 2^160, tolerances
+        that scale with max(1, |A|))
+      - integer-valued and exactly diagonal / block-diagonal matrices (zero
+        f-vectors, AlreadyDiagonal2D, exact ties)
+    """
+    rng = np.random.default_rng(seed)
+    rows = np.empty((n, 6))
+    fam = rng.integers(0, 5, n)
+    for i in range(n):
+        f = fam[i]
+        if f == 0:  # near-repeated eigenvalues under a random rotation
+            base = rng.uniform(-5, 5)
+            gap = rng.choice([0.0, 1e-15, 1e-13, 1e-11, 1e-9, 1e-6, 1e-3])
+            k = rng.integers(0, 2)
+            lam = [base, base + gap, base + rng.uniform(0.5, 3) * (1 if k else gap * 1e3)]
+            q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+            rows[i] = _pack((q * np.asarray(lam)) @ q.T)
+        elif f == 1:  # angles at the refinement / wrap boundaries
+            special = [0.0, 1e-12, 1e-8, math.pi / 8, math.pi / 4, 3 * math.pi / 8,
+                       math.pi / 2 - 1e-8, math.pi / 2]
+            phis = [rng.choice(special) * rng.choice([-1, 1]) + rng.normal(0, 1e-10) * rng.integers(0, 2)
+                    for _ in range(3)]
+            lam = np.sort(rng.uniform(-4, 4, 3))
+            rows[i] = _conj(phis, (lam[2], lam[0], lam[1]))
+        elif f == 2:  # magnitudes across the fast-path guard
+            rows[i] = rng.standard_normal(6) * 2.0 ** rng.integers(-200, 200)
+        elif f == 3:  # integer matrices (exact ties, zero f-vectors)
+            rows[i] = rng.integers(-3, 4, 6).astype(float)
+        else:  # diagonal / block-diagonal with repeated entries
+            d = rng.integers(-2, 3, 3).astype(float)
+            r = np.zeros(6)
+            r[[0, 3, 5]] = d
+            if rng.random() < 0.5:
+                r[rng.choice([1, 2, 4])] = rng.choice([1e-300, 1e-16, 0.5])
+            rows[i] = r
+    return rows
+
+
 def edge_cases_2x2() -> np.ndarray:
     rows = [[1, 0, 1], [2, 1, 2], [1, 2, 0], [3, 0, 1], [1, 0, 3], [0, 0, 0],
             [-0.0, -0.0, -0.0], [0, 1, 0], [0, -1, 0], [1, 1e-15, 1],

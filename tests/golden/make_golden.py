@@ -52,6 +52,7 @@ def main():
         "c3": workloads.generate("c3", 4096),
         "c4": workloads.generate("c4", 2048),
         "u11": np.random.default_rng(101).uniform(-1.0, 1.0, (2048, 6)),
+        "adv": cases.adversarial_3x3(4096),
     }
     for name, A in sets3.items():
         A32 = A if A.dtype == np.float32 else None

@@ -109,6 +109,9 @@ def compare3(ref: dict, got: dict, eig_tol=EIG_TOL, ang_tol=ANG_TOL, A=None) -> 
     pol = ((rs | gs) & POL) != 0
     edge = edge_window(ang_r)
     strict = gen & ~pol & ~edge
+    # gimbal lock (|phi2| -> pi/2): a polished triple is unique only up to
+    # phi1 +- phi3, so polished rows there are gated by the residual alone
+    lock = np.abs(np.abs(ang_r[:, 1]) - np.pi / 2) < 1e-2
     out = dict(
         n=n,
         code_mismatch=int((~code_ok).sum()),
@@ -128,7 +131,8 @@ def compare3(ref: dict, got: dict, eig_tol=EIG_TOL, ang_tol=ANG_TOL, A=None) -> 
         edge_rows=int((gen & ~pol & edge).sum()),
         edge_ang_max=float(ang_err[gen & ~pol & edge].max()) if (gen & ~pol & edge).any() else 0.0,
         polished_rows=int((gen & pol).sum()),
-        polished_ang_max=float(ang_err[gen & pol].max()) if (gen & pol).any() else 0.0,
+        polished_ang_max=float(ang_err[gen & pol & ~lock].max())
+        if (gen & pol & ~lock).any() else 0.0,
         degenerate_rows=int((ok_rows & (rc >= 2)).sum()),
         degenerate_ang_max=float(np.nanmax(ang_err[ok_rows & (rc >= 2)]))
         if (ok_rows & (rc >= 2)).any() else 0.0,

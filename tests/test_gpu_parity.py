@@ -68,7 +68,7 @@ def dump(name, stats):
             json.dump(stats, f, indent=1)
 
 
-@pytest.mark.parametrize("name", ["edge", "c2", "c3", "c4", "u11"])
+@pytest.mark.parametrize("name", ["edge", "c2", "c3", "c4", "u11", "adv"])
 def test_eig3_matches_reference_golden(name):
     g = load_golden(f"eig3_{name}")
     got = gpu3(g["A"])
@@ -115,6 +115,19 @@ def test_eig3_matches_oracle_large_prefix(config, n):
     # threshold; they must be rare and each must be explained (test below)
     assert_parity(stats, max_code=max(2, n // 100000), max_sign=max(2, n // 100000),
                   max_strict_fail=max(2, n // 50000))
+
+
+def test_adversarial_rows_match_oracle():
+    """2^17 seeded rows on the decision boundaries (cases.adversarial_3x3):
+    the fast path's guards must hand every ambiguous row to the literal path."""
+    from cases import adversarial_3x3
+    A = adversarial_3x3(1 << 17, seed=7200)
+    ref = O.eig3(A, report=True, nthreads=O.default_threads())
+    got = gpu3(A)
+    stats = compare3(ref, got, A=A)
+    dump("oracle_adversarial", stats)
+    assert_parity(stats, max_code=max(2, len(A) // 20000), max_sign=max(2, len(A) // 20000),
+                  max_strict_fail=max(2, len(A) // 20000))
 
 
 @pytest.mark.parametrize("config", ["c2", "c3", "c4"])
