@@ -55,6 +55,7 @@ def lib():
         L.sdo_jacobi.argtypes = [ctypes.c_int, P, I64, ctypes.c_double, P, P, P, P, P,
                                  ctypes.c_int]
         L.sdo_residuals.argtypes = [ctypes.c_int, P, P, P, I64, P]
+        L.sdo_set_nudge.argtypes = [ctypes.c_int, ctypes.c_uint64]
         L.sdo_py_hypot.argtypes = [ctypes.c_double, ctypes.c_double]
         L.sdo_py_hypot.restype = ctypes.c_double
         _lib = L
@@ -208,6 +209,17 @@ def residuals(A, lam, d, dim: int = 3):
     out = np.empty((A.shape[0], dim + 2))
     lib().sdo_residuals(dim, _p(A), _p(lam), _p(d), A.shape[0], _p(out))
     return out
+
+
+def eig3_nudged(A, mode: int, seed: int = 0, nthreads: int = 1, report: bool = False):
+    """eig3 with every libm result of the hot path moved by one ulp (mode 1
+    up, 2 down, 3 random direction per call, seeded) — the reference's own
+    sensitivity to 1-ulp libm differences."""
+    lib().sdo_set_nudge(mode, seed)
+    try:
+        return eig3(A, nthreads=nthreads, report=report)
+    finally:
+        lib().sdo_set_nudge(0, 0)
 
 
 def py_hypot(x: float, y: float) -> float:

@@ -72,7 +72,9 @@ def dump(name, stats):
 def test_eig3_matches_reference_golden(name):
     g = load_golden(f"eig3_{name}")
     got = gpu3(g["A"])
-    stats = compare3(g, got, A=g["A"])
+    # the adversarial set sits on decision boundaries by construction: every
+    # disagreement there must be explained (tests/parity.py)
+    stats = compare3(g, got, A=g["A"], explain=(name == "adv"))
     dump(f"golden_{name}", stats)
     assert_parity(stats)
 
@@ -124,10 +126,9 @@ def test_adversarial_rows_match_oracle():
     A = adversarial_3x3(1 << 17, seed=7200)
     ref = O.eig3(A, report=True, nthreads=O.default_threads())
     got = gpu3(A)
-    stats = compare3(ref, got, A=A)
+    stats = compare3(ref, got, A=A, explain=True)
     dump("oracle_adversarial", stats)
-    assert_parity(stats, max_code=max(2, len(A) // 20000), max_sign=max(2, len(A) // 20000),
-                  max_strict_fail=max(2, len(A) // 20000))
+    assert_parity(stats)
 
 
 @pytest.mark.parametrize("config", ["c2", "c3", "c4"])
