@@ -25,6 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
+    "nopool": {"PTX_POOL": 0},
     "noinline_math": {"SD_FAST_NOINLINE_MATH": 1},
 }
 
@@ -32,18 +33,23 @@ VARIANTS = {
 def build():
     from paper_1306_6291_b200 import build_ext
     OUT.mkdir(parents=True, exist_ok=True)
-    procs = []
-    for name, defs in VARIANTS.items():
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(item):
+        name, defs = item
+        defs = dict(defs)
+        pool = bool(defs.pop("PTX_POOL", 1))
         flags = [f for f in build_ext.NVCC_FLAGS if f not in ("-Xptxas", "-v")]
         cmd = [build_ext.nvcc(), *flags, *[f"-D{k}={v}" for k, v in defs.items()],
                "-o", str(OUT / f"lib_{name}.so"),
                *[str(build_ext.CSRC / s) for s in build_ext.SOURCES]]
-        procs.append((name, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
-    for name, p in procs:
-        out = p.communicate()[0]
-        if p.returncode:
-            raise SystemExit(f"{name} failed:\n{out.decode()[-3000:]}")
-        print("built", name)
+        return name, build_ext.run_nvcc(cmd, ptx_pass=pool)
+
+    with ThreadPoolExecutor(len(VARIANTS)) as ex:
+        for name, res in ex.map(one, VARIANTS.items()):
+            if res.returncode:
+                raise SystemExit(f"{name} failed:\n{(res.stdout + res.stderr)[-3000:]}")
+            print("built", name)
 
 
 def run(n: int):
