@@ -26,7 +26,6 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 VARIANTS = {
     "fast": {},
     "nopool": {"PTX_POOL": 0},
-    "noinline_math": {"SD_FAST_NOINLINE_MATH": 1},
 }
 
 
