@@ -46,6 +46,7 @@ COST = {
     "c4": dict(W=2370, bytes=48, metric_dim=3),
     "c5": dict(W=2370, bytes=96, metric_dim=3),
 }
+L2_BYTES = 126 * 1024 * 1024  # B200 L2
 METRIC = "matrices/sec (3x3 fp64 and fp32) at 1/2/4/8 B200; % of roofline"
 
 
@@ -153,8 +154,15 @@ def run_hot(sd, A, steps, warmup, config):
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
+    # working sets under 4x L2 (126 MB): overwrite a 512 MB buffer between
+    # timed calls (outside the events) so every call starts from HBM
+    moved = sum(t.numel() * t.element_size() for t in [A, *out.values()])
+    flush = torch.empty((1 << 29,), dtype=torch.uint8, device=A.device) \
+        if moved < 4 * L2_BYTES else None
     l0 = sd._lib.launch_count()
     for s, e in ev:
+        if flush is not None:
+            flush.fill_(1)
         s.record(stream)
         fn()
         e.record(stream)
@@ -162,6 +170,38 @@ def run_hot(sd, A, steps, warmup, config):
     launches = sd._lib.launch_count() - l0
     per = [s.elapsed_time(e) for s, e in ev]
     return per, launches, out
+
+
+def run_sweep(sd, dev, steps=3):
+    """sd_eig3 on N(0,1) rows at 2^20, 2^24, 2^28 and N_max
+    (HBM-filling) in fp64 and fp32 storage, device-resident."""
+    import torch
+    from paper_1306_6291_b200 import workloads
+    rows = []
+    for dt, esz, tag in ((torch.float64, 8, "f64"), (torch.float32, 4, "f32")):
+        torch.cuda.empty_cache()
+        free, _ = torch.cuda.mem_get_info(dev)
+        resident = 12 * esz + 1  # A + lam + ang + status
+        nmax = int(0.9 * free / resident) // 4096 * 4096
+        for n in (1 << 20, 1 << 24, 1 << 28, nmax):
+            t0 = time.time()
+            A = workloads.generate_torch("c5", n, dev, dtype=dt)
+            torch.cuda.synchronize()
+            gen_s = time.time() - t0
+            per, launches, out = run_hot(sd, A, steps, 2, "c5")
+            kt = statistics.median(per) * 1e-3
+            st = out["status"]
+            bad = sum(int(torch.count_nonzero((st[k:k + (1 << 26)] & 0x0F) >= 4))
+                      for k in range(0, n, 1 << 26))  # internal/deferred codes never escape
+            rows.append({"dtype": tag, "n": n, "n_is_max": n == nmax, "ms": kt * 1e3,
+                         "value": n / kt, "unit": "matrices/s",
+                         "fp64_frac": 2.0 * COST["c5"]["W"] * n / kt / 1e12,
+                         "hbm_gbs": resident * n / kt / 1e9, "gen_s": gen_s,
+                         "launches_per_call": launches / steps, "bad_status": bad})
+            log(f"[bench] sweep {tag} n={n}: {kt * 1e3:.3f} ms")
+            del A, out, st
+            torch.cuda.empty_cache()
+    return rows
 
 
 def run_e2e(sd, config, n, steps, warmup, dev_index):
@@ -311,6 +351,8 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also run the C5 size sweep (2^20 .. N_max, fp64 and fp32)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -432,10 +474,19 @@ def main():
                         "value": nc / kt, "unit": "matrices/s", "ms_per_step": kt * 1e3,
                         "fp64_roofline_frac": ach / result["roofline"]["peak"],
                         "hbm_roofline_frac": cc["bytes"] * nc / kt / 1e9
-                        / result["roofline_hbm"]["peak"]}
+                        / result["roofline_hbm"]["peak"],
+                        "l2": ("working set < 4x L2: 512 MB buffer overwritten between "
+                               "timed calls" if cc["bytes"] * nc < 4 * L2_BYTES
+                               else "inputs > L2")}
             del Ac, oc
             torch.cuda.empty_cache()
         result["configs_extra"] = extra
+    if rank == 0 and args.sweep:
+        fp = result["roofline"]["peak"]
+        sweep = run_sweep(sd, dev)
+        for r in sweep:
+            r["fp64_frac"] /= fp
+        result["sweep_c5"] = sweep
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(cfg)
     if dist is not None:

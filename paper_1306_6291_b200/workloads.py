@@ -134,12 +134,14 @@ def generate(config: str, n: int | None = None, start: int = 0) -> np.ndarray:
     return out
 
 
-def generate_torch(config: str, n: int, device, seed_offset: int = 0):
+def generate_torch(config: str, n: int, device, seed_offset: int = 0, dtype=None):
     """Same distribution as `generate`, produced on the device by torch.
 
     Used by bench.py only for batches too large to build on the host in a
     few seconds (c4 at 2^28, c5 at N_max); the values are NOT identical to
-    `generate` (different generator), the distribution is.
+    `generate` (different generator), the distribution is.  `dtype`
+    overrides the config's storage type (c5 is swept in fp64 and fp32);
+    values are always drawn in fp64 and cast once.
     """
     import torch
 
@@ -150,10 +152,17 @@ def generate_torch(config: str, n: int, device, seed_offset: int = 0):
     if config == "c1":
         return (torch.rand((n, 3), generator=g, device=device, dtype=f64)
                 * 2.0 - 1.0)
+    odt = dtype if dtype is not None else getattr(torch, spec["dtype"])
     if config in ("c2", "c5"):
-        a = torch.randn((n, 6), generator=g, device=device, dtype=f64)
-        return a.to(getattr(torch, spec["dtype"]))
-    out = torch.empty((n, 6), device=device, dtype=getattr(torch, spec["dtype"]))
+        if odt == f64 and n <= (1 << 28):
+            return torch.randn((n, 6), generator=g, device=device, dtype=f64)
+        out = torch.empty((n, 6), device=device, dtype=odt)  # chunked: N_max fills HBM
+        step = 1 << 24
+        for s in range(0, n, step):
+            m = min(step, n - s)
+            out[s:s + m] = torch.randn((m, 6), generator=g, device=device, dtype=f64)
+        return out
+    out = torch.empty((n, 6), device=device, dtype=odt)
     step = 1 << 24
     for s in range(0, n, step):
         m = min(step, n - s)

@@ -325,6 +325,43 @@ def test_full_size_properties_c2():
     assert float(res.max()) <= 1e-10
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_c5_hbm_filling_batch(dtype):
+    """SURVEY 8(d) C5 at N_max: one sd_eig3 call over a batch that fills
+    ~85% of HBM (> 2^31 rows in fp32).  Sampled rows (head, tail, seeded
+    random) against the oracle on the same values; no internal code leaks."""
+    torch.cuda.empty_cache()
+    esz = 8 if dtype == torch.float64 else 4
+    free, _ = torch.cuda.mem_get_info(DEV)
+    n = int(0.85 * free / (12 * esz + 1)) // 4096 * 4096
+    A = workloads.generate_torch("c5", n, DEV, dtype=dtype)
+    r = sd.diagonalize3_batched(A)
+    for k in range(0, n, 1 << 26):  # chunked: reductions materialise int64 temporaries
+        code = r.status[k:k + (1 << 26)] & 0x0F
+        assert int(torch.count_nonzero((code >= 4) & (code < 8))) == 0
+    rng = np.random.default_rng(55)
+    idx = np.unique(np.concatenate([np.arange(4096), np.arange(n - 4096, n),
+                                    rng.integers(0, n, 8192)]))
+    ti = torch.as_tensor(idx, device=DEV)
+    As = A[ti].cpu().numpy()
+    got = dict(lam=r.lam[ti].double().cpu().numpy(), ang=r.ang[ti].double().cpu().numpy(),
+               status=r.status[ti].cpu().numpy())
+    del A, r
+    torch.cuda.empty_cache()
+    if dtype == torch.float64:
+        ref = O.eig3(As, report=True, nthreads=O.default_threads())
+        stats = compare3(ref, got, A=As)
+        assert_parity(stats, max_code=2, max_sign=2, max_strict_fail=2)
+    else:
+        ref = O.eig3_f32(As, nthreads=O.default_threads())
+        code_mis = ((ref["status"] ^ got["status"]) & 0x0F) != 0
+        assert code_mis.sum() <= 2
+        ok = ~code_mis & ((ref["status"] & 0x0F) < 8)
+        lr = ref["lam"][ok].astype(np.float64)
+        norm = np.maximum(1.0, np.abs(lr).max(axis=1, keepdims=True))  # normwise (SURVEY H7)
+        assert (np.abs(got["lam"][ok] - lr) / norm).max() <= 1e-5
+
+
 # ---- referees (SURVEY §8f): GPU Jacobi, residuals, cubic roots ------------
 @pytest.mark.parametrize("dim", [3, 2])
 def test_jacobi_matches_reference_golden(dim):

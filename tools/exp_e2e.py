@@ -29,3 +29,20 @@ h2d = time.perf_counter() - t0
 t0 = time.perf_counter(); A.copy_(d, non_blocking=True); torch.cuda.synchronize()
 d2h = time.perf_counter() - t0
 print(json.dumps({"raw_h2d_GBps": n * 48 / h2d / 1e9, "raw_d2h_GBps": n * 48 / d2h / 1e9}))
+# concurrent H2D + D2H (the e2e pipeline's ceiling), whole buffers and chunked
+B = torch.empty((n, 6), dtype=torch.float64, pin_memory=True)
+d2 = torch.empty((n, 6), dtype=torch.float64, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for chunks in (1, 16, 64):
+    m = n // chunks
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        for c in range(chunks):
+            sl = slice(c * m, (c + 1) * m)
+            with torch.cuda.stream(s1):
+                d[sl].copy_(A[sl], non_blocking=True)
+            with torch.cuda.stream(s2):
+                B[sl].copy_(d2[sl], non_blocking=True)
+        torch.cuda.synchronize(); best = min(best, time.perf_counter() - t0)
+    print(json.dumps({"bidir_chunks": chunks, "GBps_each_way": n * 48 / best / 1e9}))
