@@ -180,7 +180,14 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     eig3_fast_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
                      T* __restrict__ ang, uint8_t* __restrict__ status) {
   constexpr int W = kFastThreads / 32;
-  constexpr bool kStoreA = kFastRows == 1;  // else phase B reloads the row (L2 hit)
+  // Phase B re-reads its row of A from global memory (an L2 hit: the block
+  // staged it moments ago) rather than parking it in shared memory: 12 KB
+  // less shared memory per block leaves more L1 for the spill traffic and
+  // measured 1-3% faster (profiles/r1_variants12_rows_storeA.jsonl).
+#ifndef SD_FAST_STORE_A
+#define SD_FAST_STORE_A 0
+#endif
+  constexpr bool kStoreA = kFastRows == 1 && SD_FAST_STORE_A;
   __shared__ __align__(16) T stage[W][32 * 6];
   __shared__ double qa[kStoreA ? 6 : 1][kStoreA ? kFastSlots : 1];
   __shared__ double ql[3][kFastSlots];
