@@ -298,6 +298,17 @@ def ncu_traffic(config):
     return None
 
 
+def ncu_fp64_pipe(config):
+    """FP64-pipe active fraction of the top kernel from the committed ncu
+    capture (profiles/ncu_summary.json), or None."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        ks = json.loads(f.read_text()).get(config, {}).get("kernels", [])
+        return ks[0]["fp64_pipe_pct"] / 100.0 if ks else None
+    except (OSError, ValueError, KeyError, AttributeError):
+        return None
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
@@ -433,6 +444,10 @@ def main():
                 "timing": "CUDA events around each sd_eig3 call on its stream; median",
                 "work_per_matrix": f"{cost['W']} FP64 instr-eq (BASELINE.md §4 cost model)",
                 "peak_source": "measured: sd_probe_dfma DFMA-chain microbenchmark, this run",
+                "ncu_fp64_pipe_active": ncu_fp64_pipe(cfg),
+                "note": ("achieved counts the reference algorithm's FP64 work W per matrix; "
+                         "the fast path executes fewer FP64 instructions than W, so frac can "
+                         "exceed 1 while the pipe itself is ncu_fp64_pipe_active busy"),
             },
             "roofline_hbm": {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak,
                              "unit": "GB/s", "frac": hbm_achieved / hbm_peak,

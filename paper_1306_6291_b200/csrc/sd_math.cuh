@@ -166,7 +166,17 @@ __device__ __forceinline__ double py_hypot(double x, double y) {
 }
 
 // math.remainder(x, pi) (exact) and the wrap helpers of core.py:29-51
+// For |x| <= pi (every angle the solver wraps) the quotient x/pi lies in
+// [-1, 1], so n = 0 for |x| <= pi/2 (x = +-pi/2 is an exact tie, rounded to
+// even 0) and n = +-1 above; x - +-pi is then exact (Sterbenz), so this is
+// bit-identical to remainder() without libdevice's general loop.
 __device__ __forceinline__ double rem_pi(Err& e, double x) {
+  const double ax = fabs(x);
+  if (ax <= 0.5 * kPi) return x;
+  if (ax <= kPi) {
+    const double r = x - copysign(kPi, x);
+    return (r == 0.0) ? copysign(0.0, x) : r;  // remainder's zero keeps x's sign
+  }
   return chk(e, remainder(x, kPi), x);
 }
 // wrap_half_pi (core.py:37-46): representative in (-pi/2, pi/2], -0 -> +0

@@ -25,9 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "nodbl": {"SD_FAST_DOUBLE_PASS": 0},
-    "nodbl_noA": {"SD_FAST_DOUBLE_PASS": 0, "SD_FAST_STORE_A": 0},
-    "dbl_rows3": {"SD_FAST_ROWS": 3},
+    "storeA": {"SD_FAST_STORE_A": 1},
 }
 
 
