@@ -55,9 +55,19 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else t.data_ptr()
 
 
-def _stream(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+def _stream(stream=None, inputs=()) -> int:
+    """Raw handle of the launch stream.  With an explicit `stream` other than
+    the current one, the launch first waits for the current stream (where
+    the inputs, and any contiguous copies of them, were produced) and the
+    inputs are recorded on `stream` so the caching allocator cannot recycle
+    them before the kernel has read them."""
+    cur = torch.cuda.current_stream()
+    if stream is None or stream == cur:
+        return cur.cuda_stream
+    stream.wait_stream(cur)
+    for t in inputs:
+        t.record_stream(stream)
+    return stream.cuda_stream
 
 
 def _check_input(A: torch.Tensor, width: int, dtypes=(torch.float64,)) -> torch.Tensor:
@@ -75,11 +85,22 @@ def _check_input(A: torch.Tensor, width: int, dtypes=(torch.float64,)) -> torch.
     return A.contiguous()
 
 
+def _same_rows(n: int, dev, *ts: torch.Tensor) -> None:
+    """Secondary inputs must match the primary one row for row and device."""
+    for t in ts:
+        if t.shape[0] != n:
+            raise ValueError(f"row count mismatch: {t.shape[0]} != {n}")
+        if t.device != dev:
+            raise ValueError(f"inputs on different devices: {t.device} != {dev}")
+
+
 def _alloc(out, key, shape, dtype, device):
     if out is not None and key in out and out[key] is not None:
         t = out[key]
-        if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous():
-            raise ValueError(f"out[{key!r}] must be contiguous {dtype} {tuple(shape)}")
+        if (tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous()
+                or t.device != device):
+            raise ValueError(f"out[{key!r}] must be a contiguous {dtype} {tuple(shape)} "
+                             f"tensor on {device}")
         return t
     return torch.empty(shape, dtype=dtype, device=device)
 
@@ -101,13 +122,13 @@ def diagonalize3_batched(A: torch.Tensor, *, report: bool = False, with_d: bool 
             rep = _alloc(out, "report", (n, REPORT_STRIDE), torch.float64, dev) if report else None
             d = _alloc(out, "d", (n, 9), torch.float64, dev) if with_d else None
             _lib.call("sd_eig3_report_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
-                      st.data_ptr(), _ptr(rep), _ptr(d), _stream(stream))
+                      st.data_ptr(), _ptr(rep), _ptr(d), _stream(stream, (A,)))
         elif dt == torch.float64:
             _lib.call("sd_eig3_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
-                      st.data_ptr(), _stream(stream))
+                      st.data_ptr(), _stream(stream, (A,)))
         else:
             _lib.call("sd_eig3_f32", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
-                      st.data_ptr(), _stream(stream))
+                      st.data_ptr(), _stream(stream, (A,)))
     return Eig3Batch(lam, ang, st, rep, d)
 
 
@@ -124,10 +145,10 @@ def diagonalize2_batched(A: torch.Tensor, *, with_d: bool = False,
         if with_d:
             d = _alloc(out, "d", (n, 4), torch.float64, dev)
             _lib.call("sd_eig2_report_f64", A.data_ptr(), n, lam.data_ptr(), phi.data_ptr(),
-                      st.data_ptr(), d.data_ptr(), _stream(stream))
+                      st.data_ptr(), d.data_ptr(), _stream(stream, (A,)))
         else:
             _lib.call("sd_eig2_f64", A.data_ptr(), n, lam.data_ptr(), phi.data_ptr(),
-                      st.data_ptr(), _stream(stream))
+                      st.data_ptr(), _stream(stream, (A,)))
     return Eig2Batch(lam, phi, st, d)
 
 
@@ -156,6 +177,7 @@ def compute_pq_batched(bcd):
 def eigenvalues3_batched(bcd, pqd):
     bcd, pqd = _check_input(bcd, 3), _check_input(pqd, 3)
     n, dev = bcd.shape[0], bcd.device
+    _same_rows(n, dev, pqd)
     lam = _empty(n, 3, dev)
     with torch.cuda.device(dev):
         _lib.call("sd_eigenvalues3_f64", bcd.data_ptr(), pqd.data_ptr(), n, lam.data_ptr(),
@@ -175,6 +197,7 @@ def pq_expanded_batched(A):
 def compute_v_batched(A, lam):
     A, lam = _check_input(A, 6), _check_input(lam, 3)
     n, dev = A.shape[0], A.device
+    _same_rows(n, dev, lam)
     v, st = _empty(n, 0, dev), _empty(n, 0, dev, torch.uint8)
     with torch.cuda.device(dev):
         _lib.call("sd_compute_v_f64", A.data_ptr(), lam.data_ptr(), n, v.data_ptr(),
@@ -186,6 +209,7 @@ def compute_w_batched(A, lam, v):
     A, lam = _check_input(A, 6), _check_input(lam, 3)
     v = _check_input(v.reshape(-1, 1), 1)
     n, dev = A.shape[0], A.device
+    _same_rows(n, dev, lam, v)
     w, st = _empty(n, 0, dev), _empty(n, 0, dev, torch.uint8)
     with torch.cuda.device(dev):
         _lib.call("sd_compute_w_f64", A.data_ptr(), lam.data_ptr(), v.data_ptr(), n,
@@ -196,6 +220,7 @@ def compute_w_batched(A, lam, v):
 def resolve_signs_batched(A, lam, vw):
     A, lam, vw = _check_input(A, 6), _check_input(lam, 3), _check_input(vw, 2)
     n, dev = A.shape[0], A.device
+    _same_rows(n, dev, lam, vw)
     ang, st, rep = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8), _empty(n, REPORT_STRIDE, dev)
     with torch.cuda.device(dev):
         _lib.call("sd_resolve_signs_f64", A.data_ptr(), lam.data_ptr(), vw.data_ptr(), n,
@@ -206,6 +231,7 @@ def resolve_signs_batched(A, lam, vw):
 def degenerate_double_batched(A, lam2):
     A, lam2 = _check_input(A, 6), _check_input(lam2, 2)
     n, dev = A.shape[0], A.device
+    _same_rows(n, dev, lam2)
     ang, st, rep = _empty(n, 3, dev), _empty(n, 0, dev, torch.uint8), _empty(n, REPORT_STRIDE, dev)
     with torch.cuda.device(dev):
         _lib.call("sd_degenerate_double_f64", A.data_ptr(), lam2.data_ptr(), n, ang.data_ptr(),
@@ -274,6 +300,7 @@ def residuals_batched(A: torch.Tensor, lam: torch.Tensor, d: torch.Tensor,
     lam = _check_input(lam.reshape(-1, dim), dim)
     d = _check_input(d.reshape(-1, dim * dim), dim * dim)
     n, dev = A.shape[0], A.device
+    _same_rows(n, dev, lam, d)
     out = _empty(n, dim + 2, dev)
     with torch.cuda.device(dev):
         _lib.call("sd_residuals_f64", dim, A.data_ptr(), lam.data_ptr(), d.data_ptr(), n,
@@ -317,21 +344,35 @@ class HostPlan:
             pass
 
     @staticmethod
-    def _hp(x):
+    def _hp(x, n, width, kinds):
+        """Pointer of a contiguous host buffer holding n*width elements of
+        one of `kinds` ("f64" / "f32" / "u8"), or ValueError."""
         if isinstance(x, torch.Tensor):
             if x.is_cuda or not x.is_contiguous():
                 raise ValueError("host buffers must be contiguous CPU tensors")
-            return x.data_ptr()
-        if not x.flags["C_CONTIGUOUS"]:
-            raise ValueError("host buffers must be C-contiguous")
-        return x.ctypes.data
+            kind = {torch.float64: "f64", torch.float32: "f32", torch.uint8: "u8"}.get(x.dtype)
+            ptr, count = x.data_ptr(), x.numel()
+        else:
+            if not x.flags["C_CONTIGUOUS"]:
+                raise ValueError("host buffers must be C-contiguous")
+            kind = {"float64": "f64", "float32": "f32", "uint8": "u8"}.get(str(x.dtype))
+            ptr, count = x.ctypes.data, x.size
+        if kind not in kinds:
+            raise TypeError(f"host buffer dtype {x.dtype} not in {kinds}")
+        if count != n * width:
+            raise ValueError(f"host buffer has {count} elements, expected {n} x {width}")
+        return ptr
 
     def eig3(self, A, lam, ang, status):
         n = A.shape[0]
-        name = "sd_eig3_f32_host" if A.dtype in (torch.float32,) or str(A.dtype) == "float32" \
-            else "sd_eig3_f64_host"
-        _lib.call(name, self._h, self._hp(A), n, self._hp(lam), self._hp(ang), self._hp(status))
+        f32 = str(A.dtype) in ("torch.float32", "float32")
+        fk = ("f32",) if f32 else ("f64",)
+        name = "sd_eig3_f32_host" if f32 else "sd_eig3_f64_host"
+        _lib.call(name, self._h, self._hp(A, n, 6, fk), n, self._hp(lam, n, 3, fk),
+                  self._hp(ang, n, 3, fk), self._hp(status, n, 1, ("u8",)))
 
     def eig2(self, A, lam, phi, status):
-        _lib.call("sd_eig2_f64_host", self._h, self._hp(A), A.shape[0], self._hp(lam),
-                  self._hp(phi), self._hp(status))
+        n = A.shape[0]
+        _lib.call("sd_eig2_f64_host", self._h, self._hp(A, n, 3, ("f64",)), n,
+                  self._hp(lam, n, 2, ("f64",)), self._hp(phi, n, 1, ("f64",)),
+                  self._hp(status, n, 1, ("u8",)))

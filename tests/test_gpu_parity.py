@@ -286,6 +286,23 @@ def test_unaligned_input_path():
     assert torch.equal(r.lam, ref.lam) and torch.equal(r.status, ref.status)
 
 
+def test_explicit_stream_and_argument_checks():
+    """stream= runs on the given stream after the producer's work (a
+    non-contiguous input is copied on the current stream first); mismatched
+    secondary inputs are rejected before launch."""
+    A = torch.as_tensor(workloads.generate("c2", 50_000)).to(DEV)
+    ref = sd.diagonalize3_batched(A)
+    At = A.t().contiguous().t()  # same values, column-major: forces a copy
+    s = torch.cuda.Stream()
+    r = sd.diagonalize3_batched(At, stream=s)
+    s.synchronize()
+    assert torch.equal(r.lam, ref.lam) and torch.equal(r.ang, ref.ang)
+    with pytest.raises(ValueError):
+        sd.compute_v_batched(A, ref.lam[:-1])
+    with pytest.raises(ValueError):
+        sd.diagonalize3_batched(A, out={"lam": torch.empty((50_000, 3), dtype=torch.float64)})
+
+
 def test_host_plan_matches_device_path():
     A = workloads.generate("c2", 300_001)
     plan = sd.HostPlan(0, chunk=1 << 16)
