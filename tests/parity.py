@@ -169,6 +169,12 @@ def compare3(ref: dict, got: dict, eig_tol=EIG_TOL, ang_tol=ANG_TOL, A=None,
         polished_mismatch=int((((rs ^ gs) & POL) != 0).sum()),
         error_rows=int(err_rows.sum()),
         error_outputs_nan=bool(nan_ok),
+        # informational: rows whose eigenvalues / angles equal the reference
+        # to the last bit (libdevice vs glibc differ by ulps)
+        lam_bit_equal_frac=float(np.all(lam_r[ok_rows] == lam_g[ok_rows], axis=1).mean())
+        if ok_rows.any() else 1.0,
+        ang_bit_equal_frac=float(np.all(ang_r[ok_rows] == ang_g[ok_rows], axis=1).mean())
+        if ok_rows.any() else 1.0,
         lam_max_err=float(np.nanmax(lam_err[ok_rows])) if ok_rows.any() else 0.0,
         lam_fail_raw=int((lam_err[ok_rows] > eig_tol).sum()),
         strict_rows=int(strict.sum()),
