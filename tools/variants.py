@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "storeA": {"SD_FAST_STORE_A": 1},
+    "gate_libm": {"SD_FAST_GATE_POLY": 0},
 }
 
 
