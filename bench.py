@@ -474,7 +474,9 @@ def main():
                              "ms_per_step": tmax * 1e3,
                              "path": "sd_eig3_f64_host: pinned host in/out, 3-stream "
                                      "chunked H2D/kernel/D2H pipeline"}
-    if rank == 0 and not args.no_extra and args.n == 0:
+    # extras and the CPU baseline: rank 0 of a 1-GPU run only (the scaling
+    # runs report the headline metric)
+    if rank == 0 and world == 1 and not args.no_extra and args.n == 0:
         extra = {}
         for c in ("c1", "c3", "c4"):
             if c == cfg:
@@ -502,7 +504,7 @@ def main():
         for r in sweep:
             r["fp64_frac"] /= fp
         result["sweep_c5"] = sweep
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(cfg)
     if dist is not None:
         dist.barrier()
