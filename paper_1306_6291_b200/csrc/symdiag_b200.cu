@@ -219,8 +219,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
             ang[3 * i + k] = (T)0.0;
           }
           // fp32 outputs cannot carry the closed form into the polish: literal
-          status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT
-                                 : (sizeof(T) == 8 ? sd::kPolishTriple : sd::kDeferred);
+          status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT : sd::kPolishTriple;
         } else if (cls == 2) {
           status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
         }
@@ -280,17 +279,16 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     const double scale = sd::fast_scale(g);
     const int rc = is_gen ? sd::fast_generic(g, scale, gl, phi, st)
                           : sd::fast_double(g, scale, gl, phi, st);
-    if (rc == sd::kFastDone || (rc == sd::kFastPolish && sizeof(T) == 8)) {
-      // done, or (fp64) closed form written with the polish pending
+    if (rc == sd::kFastDone || rc == sd::kFastPolish) {
+      // done, or closed form written with the polish pending (fp32: the
+      // polish pass recomputes the fp64 closed form itself)
 #pragma unroll
       for (int k = 0; k < 3; k++) {
         lam[3 * r + k] = (T)gl[k];
         ang[3 * r + k] = (T)phi[k];
       }
-      status[r] = st;
-    } else {
-      status[r] = (rc == sd::kFastPolish) ? (uint8_t)(sd::kDeferred | (11 << 4)) : st;
     }
+    status[r] = st;  // branch code, kPolish*, or kDeferred with its reason
   }
 }
 
@@ -328,9 +326,38 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
     }
     status[i] = r.status;
   } else {
-    const uint8_t st = status[i];
-    const double lm[3] = {(double)lam[3 * i], (double)lam[3 * i + 1], (double)lam[3 * i + 2]};
-    double ph[3] = {(double)ang[3 * i], (double)ang[3 * i + 1], (double)ang[3 * i + 2]};
+    uint8_t st = status[i];
+    double lm[3], ph[3];
+    if (sizeof(T) == 8) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        lm[q] = (double)lam[3 * i + q];
+        ph[q] = (double)ang[3 * i + q];
+      }
+    } else {
+      // fp32 outputs cannot carry the fp64 closed form from the fast kernel:
+      // recompute it here (same code, same inputs, same result)
+      double scale = 1.0;
+      int reason = 0, rc = sd::kFastDefer;
+      const int cls = sd::classify3(a, lm, scale, reason);
+      if (cls == 4) {
+        ph[0] = ph[1] = ph[2] = 0.0;
+        rc = sd::kFastPolish;
+      } else if (cls == 0) {
+        rc = sd::fast_generic(a, scale, lm, ph, st);
+      } else if (cls == 3) {
+        rc = sd::fast_double(a, scale, lm, ph, st);
+      }
+      if (rc != sd::kFastPolish) {  // cannot happen; the literal pass is the safety net
+        status[i] = (uint8_t)(sd::kDeferred | (11 << 4));
+        return;
+      }
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        lam[3 * i + q] = (T)lm[q];
+        ang[3 * i + q] = (T)ph[q];
+      }
+    }
     uint8_t code = SD_CODE_GENERIC;
     if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
     if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
