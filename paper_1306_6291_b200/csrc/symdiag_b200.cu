@@ -287,6 +287,9 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
         lam[3 * r + k] = (T)gl[k];
         ang[3 * r + k] = (T)phi[k];
       }
+    } else if (rc == sd::kFastError) {
+#pragma unroll
+      for (int k = 0; k < 3; k++) lam[3 * r + k] = ang[3 * r + k] = (T)sd::qnan();
     }
     status[r] = st;  // branch code, kPolish*, or kDeferred with its reason
   }
