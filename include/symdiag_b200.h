@@ -176,8 +176,9 @@ int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots,
 
 /* ---- host-buffer path (end-to-end: H2D, kernel, D2H, pipelined) ---------- */
 typedef struct sd_plan sd_plan;
-/* A plan owns device staging buffers for `chunk` matrices (double-buffered)
- * and two CUDA streams on `device`.                                         */
+/* A plan owns three device staging slots of `chunk` matrices and three CUDA
+ * streams on `device` (copy-in / compute / copy-out of neighbouring chunks
+ * overlap).                                                                 */
 int sd_plan_create(int device, int64_t chunk, sd_plan** out);
 int sd_plan_destroy(sd_plan* plan);
 /* Host-memory variants of sd_eig3_f64 / sd_eig3_f32 / sd_eig2_f64.  Copies
@@ -189,6 +190,32 @@ int sd_eig3_f32_host(sd_plan* plan, const float* A, int64_t n, float* lam,
                      float* ang, uint8_t* status);
 int sd_eig2_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
                      double* phi, uint8_t* status);
+
+/* ---- JSON-lines codec of the `solve` front end (host only, no CUDA) -------
+ * Replaces the per-record json.loads / dumps of the reference CLI
+ * (cli.py:51-80 parse_record, cli.py:33-48 + 83-114 result records).      */
+/* Split buf[0, len) into lines, drop blank ones (str.strip semantics for
+ * ASCII) and parse up to `cap` of them with `nthreads` host threads.  Per
+ * line k: kind[k] = 3 or 2 with rows[6k ..] = packed (a11,a12,a13,a22,a23,a33)
+ * or (a11,a12,a22); or 0 when the line is not a record this parser can read
+ * exactly like json.loads + parse_record (malformed, non-finite, non-numeric,
+ * duplicate or unexpected keys, escaped / non-ASCII id, ...): the caller
+ * parses it.  span[4k ..] = line begin, end, id token begin, end (-1: id
+ * absent or null); offsets into buf.  Returns the line count (< 0 on bad
+ * arguments); *consumed = bytes of buf covered by those lines.              */
+int64_t sd_jsonl_parse(const char* buf, int64_t len, int64_t cap, int nthreads,
+                       int8_t* kind, double* rows, int64_t* span, int64_t* consumed);
+/* Format ResultRecords (one per line, '\n'-terminated) for records k with
+ * dim[k] in {2, 3}; dim[k] = 0 skips k (offsets[k] == offsets[k+1]).  Per
+ * record: id token idbuf[id_span[2k], id_span[2k+1]) or null, lam[3k ..],
+ * ang[3k ..] (2x2: phi at ang[3k]), d[9k ..] row-major D (2x2: 4 values),
+ * res[5k ..] = (recon_rel, ortho, eigvec residuals), status[k] (branch).
+ * Returns the byte count written to out, -(needed) if out_cap is too small,
+ * or -1 on bad arguments; offsets[n+1] receives record boundaries.         */
+int64_t sd_jsonl_format(int64_t n, const int8_t* dim, const char* idbuf,
+                        const int64_t* id_span, const double* lam, const double* ang,
+                        const double* d, const double* res, const uint8_t* status,
+                        int nthreads, char* out, int64_t out_cap, int64_t* offsets);
 
 /* ---- diagnostics --------------------------------------------------------- */
 /* sd_eig3_f64 evaluated entirely in the reference's literal evaluation

@@ -39,6 +39,8 @@ SIGNATURES = {
     "sd_residuals_f64": [_I, _P, _P, _P, _I64, _P, _P],
     "sd_cubic_roots_f64": [_P, _I64, _P, _P, _P],
     "sd_plan_create": [_I, _I64, ctypes.POINTER(_P)],
+    "sd_jsonl_parse": [_P, _I64, _I64, _I, _P, _P, _P, _P],
+    "sd_jsonl_format": [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I64, _P],
     "sd_plan_destroy": [_P],
     "sd_eig3_f64_host": [_P, _P, _I64, _P, _P, _P],
     "sd_eig3_f32_host": [_P, _P, _I64, _P, _P, _P],
@@ -51,7 +53,8 @@ SIGNATURES = {
     "sd_launch_count": [],
 }
 RESTYPES = {"sd_last_error": ctypes.c_char_p, "sd_version": ctypes.c_char_p,
-            "sd_launch_count": ctypes.c_int64}
+            "sd_launch_count": ctypes.c_int64, "sd_jsonl_parse": ctypes.c_int64,
+            "sd_jsonl_format": ctypes.c_int64}
 
 
 class CudaUnavailable(RuntimeError):

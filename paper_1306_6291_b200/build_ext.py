@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libsymdiag_b200.so"
-SOURCES = ["symdiag_b200.cu", "sd_host.cu"]
+SOURCES = ["symdiag_b200.cu", "sd_host.cu", "sd_jsonl.cpp"]
 # PTX pass between cicc and ptxas (ptx_constpool.py); SD_PTX_POOL=0 disables
 PTX_POOL = os.environ.get("SD_PTX_POOL", "1") != "0"
 HEADERS = ["sd_math.cuh", "sd_eig3.cuh", "sd_eig2.cuh", "sd_fast3.cuh", "sd_jacobi.cuh"]

@@ -146,3 +146,61 @@ def test_cli_bench_reports_ratio():
     assert cli.cmd_bench(out, 100_000, 42) == 0
     r = json.loads(out.getvalue())
     assert r["n"] == 100_000 and r["throughput_ratio_closed_over_jacobi"] > 0
+
+
+def _both(text, **kw):
+    """(rc, output, exception type) of the Python front end and the native
+    codec on the same input."""
+    res = []
+    for fn in (cli.cmd_solve, cli.cmd_solve_native):
+        out = io.StringIO()
+        try:
+            rc, exc = fn(io.StringIO(text), out, **kw), None
+        except Exception as e:  # noqa: BLE001 — compared below
+            rc, exc = None, type(e)
+        res.append((rc, out.getvalue(), exc))
+    return res
+
+
+def _mixed_corpus(n=3000, seed=5):
+    rng = np.random.default_rng(seed)
+    lines = []
+    for k in range(n):
+        r = rng.random()
+        if r < 0.6:
+            v = rng.standard_normal(6)
+            lines.append(json.dumps({"id": f"m{k}", "a11": v[0], "a22": v[1], "a33": v[2],
+                                     "a12": v[3], "a13": v[4], "a23": v[5]}))
+        elif r < 0.8:
+            v = rng.uniform(-1, 1, 3)
+            lines.append(json.dumps({"a11": v[0], "a22": v[1], "a12": v[2]}))
+        elif r < 0.85:
+            lines.append(json.dumps({"id": "é\n", "a11": 1.0, "a22": 2.0, "a12": 0.5}))
+        elif r < 0.9:
+            lines.append(["{bad", "{}", '{"a11": NaN, "a22": 1, "a12": 0}', "", "  "][k % 5])
+        else:  # rotated degenerate / diagonal / integer matrices
+            lines.append('{"id": "d%d", "a11": 2, "a22": 2, "a33": 2, "a12": 0, "a13": 0, '
+                         '"a23": 0}' % k)
+    return "\n".join(lines) + "\n"
+
+
+@gpu
+def test_native_codec_solve_is_byte_identical():
+    """cmd_solve_native (C++ codec) writes exactly what cmd_solve writes: the
+    golden corpus, a mixed stream with parse errors, blank lines, escaped
+    ids and 2x2/3x3 records, with and without --inline-errors."""
+    for text in ((GOLDEN / "cli_solve_input.jsonl").read_text(), _mixed_corpus()):
+        for kw in ({}, {"inline_errors": True}, {"batch": 257}):
+            (rc_p, out_p, ex_p), (rc_n, out_n, ex_n) = _both(text, **kw)
+            assert (rc_p, ex_p) == (rc_n, ex_n)
+            assert out_p == out_n
+
+
+@gpu
+def test_native_codec_solver_exception_prefix():
+    text = ('{"id": "ok", "a11": 1, "a22": 2, "a33": 3, "a12": 0.1, "a13": 0.2, "a23": 0.3}\n'
+            '{"bad json\n'
+            '{"id": "big", "a11": 1e200, "a22": 2, "a33": 3, "a12": 0, "a13": 0, "a23": 0}\n'
+            '{"id": "after", "a11": 1, "a22": 2, "a12": 0.5}\n')
+    (rc_p, out_p, ex_p), (rc_n, out_n, ex_n) = _both(text)
+    assert ex_p is ex_n is OverflowError and out_p == out_n and len(out_n.splitlines()) == 2
