@@ -204,3 +204,24 @@ def test_native_codec_solver_exception_prefix():
             '{"id": "after", "a11": 1, "a22": 2, "a12": 0.5}\n')
     (rc_p, out_p, ex_p), (rc_n, out_n, ex_n) = _both(text)
     assert ex_p is ex_n is OverflowError and out_p == out_n and len(out_n.splitlines()) == 2
+
+
+@gpu
+def test_native_verify_matches_python_verify():
+    from paper_1306_6291_b200 import workloads
+    rows = workloads.generate("c2", 3000)
+    recs = [json.dumps({"id": f"v{k}", "a11": r[0], "a22": r[3], "a33": r[5], "a12": r[1],
+                        "a13": r[2], "a23": r[4]}) for k, r in enumerate(rows)]
+    recs += [json.dumps({"a11": 0.5, "a22": -1.0, "a12": 0.25})] * 5
+    text = "\n".join(recs) + "\n"
+    for corrupt in (False, True):
+        outs = []
+        for fn in (cli.cmd_verify, cli.cmd_verify_native):
+            out = io.StringIO()
+            rc = fn(io.StringIO(text), out, 1e-9, corrupt=corrupt)
+            outs.append((rc, out.getvalue()))
+        assert outs[0] == outs[1]
+    bad = text + "{oops\n"
+    for fn in (cli.cmd_verify, cli.cmd_verify_native):
+        with pytest.raises(cli.ParseError):
+            fn(io.StringIO(bad), io.StringIO(), 1e-9)
