@@ -190,6 +190,14 @@ int sd_eig3_f32_host(sd_plan* plan, const float* A, int64_t n, float* lam,
                      float* ang, uint8_t* status);
 int sd_eig2_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
                      double* phi, uint8_t* status);
+/* Synchronous host-buffer sd_eig3_report_f64 / sd_eig2_report_f64 (report /
+ * d may be NULL): the low-latency path of the reference-style scalar calls
+ * (diagonalize3(SymMat3), diagonalize2(SymMat2)).  Host buffers may be
+ * pageable.                                                                 */
+int sd_eig3_report_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
+                            double* ang, uint8_t* status, double* report, double* d);
+int sd_eig2_report_f64_host(sd_plan* plan, const double* A, int64_t n, double* lam,
+                            double* phi, uint8_t* status, double* d);
 
 /* ---- JSON-lines codec of the `solve` front end (host only, no CUDA) -------
  * Replaces the per-record json.loads / dumps of the reference CLI

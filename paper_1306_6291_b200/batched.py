@@ -376,3 +376,51 @@ class HostPlan:
         _lib.call("sd_eig2_f64_host", self._h, self._hp(A, n, 3, ("f64",)), n,
                   self._hp(lam, n, 2, ("f64",)), self._hp(phi, n, 1, ("f64",)),
                   self._hp(status, n, 1, ("u8",)))
+
+
+# ---- low-latency path of the reference-style scalar calls -----------------
+_scalar_plans: dict = {}
+_scalar_lock = __import__("threading").Lock()
+
+
+def _scalar_plan():
+    """One small HostPlan per device (lazily), shared by scalar calls under a
+    lock (the reference's values are safe to use from several threads)."""
+    _lib.require_cuda()
+    dev = torch.cuda.current_device()
+    plan = _scalar_plans.get(dev)
+    if plan is None:
+        plan = _scalar_plans[dev] = HostPlan(dev, chunk=1024)
+    return plan
+
+
+def eig3_report_host(A, report: bool = True, with_d: bool = True):
+    """sd_eig3_report_f64_host on host rows A[n,6] -> numpy (lam, ang,
+    status, report | None, d | None); one synchronous C call."""
+    import numpy as np
+    A = np.ascontiguousarray(A, np.float64).reshape(-1, 6)
+    n = A.shape[0]
+    lam, ang = np.empty((n, 3)), np.empty((n, 3))
+    st = np.empty(n, np.uint8)
+    rep = np.empty((n, REPORT_STRIDE)) if report else None
+    d = np.empty((n, 9)) if with_d else None
+    with _scalar_lock:
+        plan = _scalar_plan()
+        _lib.call("sd_eig3_report_f64_host", plan._h, A.ctypes.data, n, lam.ctypes.data,
+                  ang.ctypes.data, st.ctypes.data, None if rep is None else rep.ctypes.data,
+                  None if d is None else d.ctypes.data)
+    return lam, ang, st, rep, d
+
+
+def eig2_report_host(A, with_d: bool = True):
+    """sd_eig2_report_f64_host on host rows A[n,3] = (a11, a12, a22)."""
+    import numpy as np
+    A = np.ascontiguousarray(A, np.float64).reshape(-1, 3)
+    n = A.shape[0]
+    lam, phi, st = np.empty((n, 2)), np.empty(n), np.empty(n, np.uint8)
+    d = np.empty((n, 4)) if with_d else None
+    with _scalar_lock:
+        plan = _scalar_plan()
+        _lib.call("sd_eig2_report_f64_host", plan._h, A.ctypes.data, n, lam.ctypes.data,
+                  phi.ctypes.data, st.ctypes.data, None if d is None else d.ctypes.data)
+    return lam, phi, st, d

@@ -172,17 +172,15 @@ def degenerate_double(a: SymMat3, lam, lam3):
 
 def diagonalize3(a: SymMat3) -> EigenDecomp3:
     """diagonalize3 (eig3.py:509-565) through the fused B200 kernel."""
-    res = batched.diagonalize3_batched(_a(a), report=True, with_d=True)
-    st = int(res.status[0].item())
+    lam, ang, st, rep, d = batched.eig3_report_host([a.packed()])  # one synchronous C call
+    st = int(st[0])
     c = st & S.CODE_MASK
     if c >= S.ERR_FIRST:
         S.raise_for(c, "diagonalize3")
-    lam = res.lam[0].tolist()
-    rep = res.report[0].cpu().numpy()
-    return EigenDecomp3(lambda1=lam[0], lambda2=lam[1], lambda3=lam[2],
-                        angles=Angles3(*res.ang[0].tolist()),
-                        d=res.d[0].cpu().numpy().reshape(3, 3),
-                        branch=_BRANCH[c], report=_report_from_row(st, rep))
+    l1, l2, l3 = lam[0].tolist()
+    return EigenDecomp3(lambda1=l1, lambda2=l2, lambda3=l3, angles=Angles3(*ang[0].tolist()),
+                        d=d[0].reshape(3, 3), branch=_BRANCH[c],
+                        report=_report_from_row(st, rep[0]))
 
 
 def euler_angles(dec: EigenDecomp3) -> Angles3:

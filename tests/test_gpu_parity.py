@@ -463,3 +463,39 @@ def test_referee_scalar_api():
     r2 = sd.jacobi_eigen(sd.SymMat2(1.0, 0.0, 2.0))  # (a11, a22, a12): (1 +- sqrt 17) / 2
     assert np.allclose(np.sort(r2.eigenvalues), [(1 - 17 ** 0.5) / 2, (1 + 17 ** 0.5) / 2],
                        atol=1e-13)
+
+
+def test_scalar_api_matches_batched_and_raises_like_reference():
+    """The reference-style scalar calls (one synchronous host-buffer call
+    each) return exactly the report kernel's rows, and raise the reference's
+    exceptions on error rows."""
+    g = load_golden("eig3_edge")
+    A = g["A"]
+    batch = sd.diagonalize3_batched(torch.as_tensor(A).to(DEV), report=True, with_d=True)
+    torch.cuda.synchronize()
+    lam, ang, st = batch.lam.cpu().numpy(), batch.ang.cpu().numpy(), batch.status.cpu().numpy()
+    d = batch.d.cpu().numpy()
+    for k, row in enumerate(A):
+        if (st[k] & 0x0F) >= 8:
+            with pytest.raises(Exception):  # at SymMat3 construction or in the solve
+                sd.diagonalize3(sd.SymMat3(row[0], row[3], row[5], row[1], row[2], row[4]))
+            continue
+        m = sd.SymMat3(row[0], row[3], row[5], row[1], row[2], row[4])
+        dec = sd.diagonalize3(m)
+        assert list(dec.lambdas) == lam[k].tolist()
+        assert [dec.angles.phi1, dec.angles.phi2, dec.angles.phi3] == ang[k].tolist()
+        assert np.array_equal(dec.d.reshape(-1), d[k])
+    g2 = load_golden("eig2_c1")
+    A2 = g2["A"][:300]
+    b2 = sd.diagonalize2_batched(torch.as_tensor(A2).to(DEV), with_d=True)
+    torch.cuda.synchronize()
+    st2 = b2.status.cpu().numpy()
+    for k, (a11, a12, a22) in enumerate(A2):
+        if (st2[k] & 0x0F) >= 8:
+            with pytest.raises(Exception):
+                sd.diagonalize2(sd.SymMat2(a11, a22, a12))
+            continue
+        dec = sd.diagonalize2(sd.SymMat2(a11, a22, a12))
+        assert [dec.lambda1, dec.lambda2] == b2.lam[k].tolist()
+        assert dec.phi == b2.phi[k].item()
+        assert np.array_equal(dec.d.reshape(-1), b2.d[k].cpu().numpy())
