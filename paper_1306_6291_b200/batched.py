@@ -424,3 +424,38 @@ def eig2_report_host(A, with_d: bool = True):
         _lib.call("sd_eig2_report_f64_host", plan._h, A.ctypes.data, n, lam.ctypes.data,
                   phi.ctypes.data, st.ctypes.data, None if d is None else d.ctypes.data)
     return lam, phi, st, d
+
+
+def diagonalize3_host_multi(A, lam, ang, status, devices=None, chunk: int = 1 << 20):
+    """One process, several GPUs: host rows A[n,6] (fp64 or
+    fp32) are cut into contiguous shards, one per entry of `devices`
+    (default: every visible GPU), and each shard runs through its own
+    HostPlan (3-stream copy/compute pipeline) on its own host thread; the
+    ctypes calls release the GIL, so the shards' PCIe links and GPUs work
+    concurrently.  No collective: outputs land in the caller's host buffers."""
+    import threading
+    from .shard import shard_range
+    _lib.require_cuda()
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    n, world = A.shape[0], len(devices)
+    plans = [HostPlan(dev, chunk=chunk) for dev in devices]
+    errors = []
+
+    def work(r):
+        a, b = shard_range(n, r, world)
+        try:
+            if b > a:
+                plans[r].eig3(A[a:b], lam[a:b], ang[a:b], status[a:b])
+        except Exception as e:  # noqa: BLE001 — re-raised below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for p in plans:
+        p.close()
+    if errors:
+        raise errors[0]

@@ -499,3 +499,18 @@ def test_scalar_api_matches_batched_and_raises_like_reference():
         assert [dec.lambda1, dec.lambda2] == b2.lam[k].tolist()
         assert dec.phi == b2.phi[k].item()
         assert np.array_equal(dec.d.reshape(-1), b2.d[k].cpu().numpy())
+
+
+def test_single_process_multi_device_host_path():
+    """diagonalize3_host_multi: contiguous shards on concurrent host threads,
+    one HostPlan each (two on the same GPU here; one per GPU on a node),
+    equal to the single-call result bit for bit."""
+    A = workloads.generate("c2", 300_001)
+    ref = sd.diagonalize3_batched(torch.as_tensor(A).to(DEV))
+    torch.cuda.synchronize()
+    lam, ang = np.empty((A.shape[0], 3)), np.empty((A.shape[0], 3))
+    st = np.empty(A.shape[0], np.uint8)
+    sd.diagonalize3_host_multi(A, lam, ang, st, devices=[0, 0, 0], chunk=1 << 16)
+    assert np.array_equal(lam, ref.lam.cpu().numpy())
+    assert np.array_equal(ang, ref.ang.cpu().numpy())
+    assert np.array_equal(st, ref.status.cpu().numpy())
