@@ -514,3 +514,52 @@ def test_single_process_multi_device_host_path():
     assert np.array_equal(lam, ref.lam.cpu().numpy())
     assert np.array_equal(ang, ref.ang.cpu().numpy())
     assert np.array_equal(st, ref.status.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [1, 31, 257, 4099])
+def test_no_writes_outside_outputs(n):
+    """Out-of-bounds write check (compute-sanitizer is not available on the
+    pool): every output is a window of a larger buffer whose guard bands hold
+    a sentinel; after each entry point the guards must be untouched."""
+    G = 4096  # guard elements on each side
+    A = torch.as_tensor(workloads.generate("c3", n).astype(np.float64)).to(DEV)
+
+    def window(shape, dtype):
+        numel = int(np.prod(shape))
+        buf = torch.full((numel + 2 * G,), 0x5A if dtype == torch.uint8 else -7.25e30,
+                         dtype=dtype, device=DEV)
+        return buf, buf[G:G + numel].view(*shape)
+
+    def check(buf, dtype):
+        s = 0x5A if dtype == torch.uint8 else -7.25e30
+        assert bool((buf[:G] == s).all()) and bool((buf[-G:] == s).all())
+
+    for dt in (torch.float64, torch.float32):
+        bl, lam = window((n, 3), dt)
+        ba, ang = window((n, 3), dt)
+        bs, st = window((n,), torch.uint8)
+        sd.diagonalize3_batched(A.to(dt), out={"lam": lam, "ang": ang, "status": st})
+        torch.cuda.synchronize()
+        for b, t in ((bl, dt), (ba, dt), (bs, torch.uint8)):
+            check(b, t)
+    bl, lam = window((n, 3), torch.float64)
+    ba, ang = window((n, 3), torch.float64)
+    bs, st = window((n,), torch.uint8)
+    br, rep = window((n, 24), torch.float64)
+    bd, dm = window((n, 9), torch.float64)
+    sd.diagonalize3_batched(A, report=True, with_d=True,
+                            out={"lam": lam, "ang": ang, "status": st, "report": rep, "d": dm})
+    torch.cuda.synchronize()
+    for b, t in ((bl, torch.float64), (ba, torch.float64), (bs, torch.uint8),
+                 (br, torch.float64), (bd, torch.float64)):
+        check(b, t)
+    A2 = torch.as_tensor(workloads.generate("c1", n)).to(DEV)
+    bl, lam = window((n, 2), torch.float64)
+    bp, phi = window((n,), torch.float64)
+    bs, st = window((n,), torch.uint8)
+    bd, dm = window((n, 4), torch.float64)
+    sd.diagonalize2_batched(A2, with_d=True, out={"lam": lam, "phi": phi, "status": st, "d": dm})
+    torch.cuda.synchronize()
+    for b, t in ((bl, torch.float64), (bp, torch.float64), (bs, torch.uint8),
+                 (bd, torch.float64)):
+        check(b, t)
