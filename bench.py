@@ -62,6 +62,66 @@ def peaks():
     return p
 
 
+class NvmlClockSampler:
+    """SM clock and clock-event reasons polled through NVML every ~1 ms on a
+    background thread while the timed region runs (nvidia-smi's 20 ms loop
+    yields only one or two samples in a ~20 ms region)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, cuda_index: int):
+        import pynvml
+        import torch
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(cuda_index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001 — older torch / driver: fall back to the index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
+        self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        self.samples, self.masks = [], 0
+        self.run = False
+
+    def _poll(self):
+        nv = self.nv
+        while self.run:
+            self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+            self.masks |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            time.sleep(0.001)
+
+    def __enter__(self):
+        self.run = True
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 1.0:
+            time.sleep(0.0005)
+        return self
+
+    def __exit__(self, *exc):
+        self.run = False
+        self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = [n for n, attr in self.REASONS if self.masks & getattr(self.nv, attr)]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, ~1 ms"}
+
+
+def clock_sampler(cuda_index: int):
+    try:
+        return NvmlClockSampler(cuda_index)
+    except Exception:  # noqa: BLE001 — no NVML bindings: nvidia-smi loop
+        return ClockSampler(cuda_index)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -400,7 +460,7 @@ def main():
         torch.cuda.synchronize()
 
     barrier()
-    with ClockSampler(dev.index) as clk:
+    with clock_sampler(dev.index) as clk:
         barrier()
         per, launches, out = run_hot(sd, A, args.steps, args.warmup, cfg)
         barrier()
