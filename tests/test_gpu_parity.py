@@ -8,6 +8,7 @@ degeneracies, identical branch and sign choices; fp32 1e-5 relative.
 
 from __future__ import annotations
 
+import io
 import json
 import os
 
@@ -563,3 +564,25 @@ def test_no_writes_outside_outputs(n):
     for b, t in ((bl, torch.float64), (bp, torch.float64), (bs, torch.uint8),
                  (bd, torch.float64)):
         check(b, t)
+
+
+def test_empty_batches():
+    """n = 0 through every batched entry point and the host paths: empty
+    outputs, no launch error."""
+    e6 = torch.empty((0, 6), dtype=torch.float64, device=DEV)
+    e3 = torch.empty((0, 3), dtype=torch.float64, device=DEV)
+    for r in (sd.diagonalize3_batched(e6), sd.diagonalize3_batched(e6.float()),
+              sd.diagonalize3_batched(e6, report=True, with_d=True)):
+        assert r.lam.shape == (0, 3) and r.status.shape == (0,)
+    r2 = sd.diagonalize2_batched(e3, with_d=True)
+    assert r2.lam.shape == (0, 2) and r2.phi.shape == (0,)
+    assert sd.jacobi_batched(e6).evals.shape == (0, 3)
+    assert sd.compose_rotation_batched(e3).shape == (0, 9)
+    plan = sd.HostPlan(0, chunk=1 << 10)
+    z = np.empty((0, 6))
+    plan.eig3(z, np.empty((0, 3)), np.empty((0, 3)), np.empty(0, np.uint8))
+    plan.close()
+    from paper_1306_6291_b200 import cli
+    out = io.StringIO()
+    assert cli.cmd_solve_native(io.StringIO(""), out) == 0 and out.getvalue() == ""
+    torch.cuda.synchronize()
