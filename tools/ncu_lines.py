@@ -21,7 +21,9 @@ import sys
 import tempfile
 from pathlib import Path
 
-LIB = Path(__file__).resolve().parents[1] / "paper_1306_6291_b200" / "lib" / "libsymdiag_b200.so"
+import os
+LIB = Path(os.environ.get("SD_LIB", Path(__file__).resolve().parents[1] / "paper_1306_6291_b200"
+                         / "lib" / "libsymdiag_b200.so"))
 
 
 def line_table(fun_sub: str):
