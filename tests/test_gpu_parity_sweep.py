@@ -85,3 +85,31 @@ def test_parity_sweep_2x2():
     assert worst <= 1e-15
     _dump("sweep_c1", {"rows": N * K, "status_equal": True, "lam_bit_equal": True,
                        "phi_max_diff": worst})
+
+
+def test_parity_sweep_fp32_c4():
+    """fp32 storage (sd_eig3_f32) vs the oracle's fp32 entry point: same
+    status except rows a threshold decides within rounding (<= 1 per 10^6),
+    eigenvalues within 1e-5 normwise, non-polished Generic angles within
+    1e-5."""
+    mis = rows = 0
+    worst_l = worst_a = 0.0
+    for k in range(K):
+        A32 = workloads.generate("c4", N, start=(k + 1) << 26)
+        ref = O.eig3_f32(A32, nthreads=O.default_threads())
+        r = sd.diagonalize3_batched(torch.as_tensor(A32).to(DEV))
+        torch.cuda.synchronize()
+        st, lam, ang = r.status.cpu().numpy(), r.lam.cpu().numpy(), r.ang.cpu().numpy()
+        code_ok = ((st ^ ref["status"]) & 0x0F) == 0
+        mis += int((~code_ok).sum())
+        ok = code_ok & ((ref["status"] & 0x0F) < 8)
+        lr = ref["lam"][ok].astype(np.float64)
+        norm = np.maximum(1.0, np.abs(lr).max(axis=1, keepdims=True))
+        worst_l = max(worst_l, float((np.abs(lam[ok] - lr) / norm).max()))
+        gen = ok & ((ref["status"] & 0x0F) == 0) & (((ref["status"] | st) & 0x80) == 0)
+        worst_a = max(worst_a, float(wrapped_diff(ang[gen], ref["ang"][gen]).max()))
+        rows += N
+    assert mis <= max(2, rows // 1_000_000)
+    assert worst_l <= 1e-5 and worst_a <= 1e-5
+    _dump("sweep_c4_fp32", {"rows": rows, "code_mismatch": mis, "lam_max_err_normwise": worst_l,
+                            "generic_ang_max": worst_a})
