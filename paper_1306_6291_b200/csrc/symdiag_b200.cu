@@ -464,31 +464,22 @@ __global__ void __launch_bounds__(kThreads) eig2_kernel(const double* __restrict
                                                         double* __restrict__ phi,
                                                         uint8_t* __restrict__ status,
                                                         double* __restrict__ dmat) {
-  __shared__ __align__(16) double sm[kWarps][32 * 3 + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * 32;
-  if (row0 >= n) return;
-  // 3 values per row: odd width, so stage element-wise (still coalesced)
-  const int rows = warp_stage<double, 3, false>(A, n, row0, sm[warp]);
-  (void)kVec;
-  double l1 = 0.0, l2 = 0.0, ph = 0.0;
-  uint8_t st = 0;
-  if (lane < rows) {
-    const double* p = sm[warp] + 3 * lane;
-    st = sd::diagonalize2(p[0], p[1], p[2], l1, l2, ph);
+  // One row per thread, no shared-memory staging: the warp's three 8-byte
+  // loads per row cover the same 768 contiguous bytes (L1 serves the second
+  // and third), and (l1, l2) leaves as one 16-byte store per lane, a
+  // contiguous 512-byte warp store when lam is 16-byte aligned (kVec).
+  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  const double* p = A + 3 * i;
+  double l1, l2, ph;
+  const uint8_t st = sd::diagonalize2(__ldg(p), __ldg(p + 1), __ldg(p + 2), l1, l2, ph);
+  if (kVec) {
+    reinterpret_cast<double2*>(lam)[i] = make_double2(l1, l2);
+  } else {
+    lam[2 * i] = l1;
+    lam[2 * i + 1] = l2;
   }
-  __syncwarp();
-  // stage (l1, l2) for a coalesced store of the [rows][2] block
-  double* so = sm[warp];
-  if (lane < rows) {
-    so[2 * lane] = l1;
-    so[2 * lane + 1] = l2;
-  }
-  __syncwarp();
-  double* dst = lam + 2 * row0;
-  for (int j = lane; j < 2 * rows; j += 32) dst[j] = so[j];
-  if (lane < rows) {
-    const int64_t i = row0 + lane;
+  {
     phi[i] = ph;
     status[i] = st;
     if (kReport && dmat) {
@@ -811,7 +802,10 @@ int launch_eig2(const double* A, int64_t n, double* lam, double* phi, uint8_t* s
   if (n < 0 || (n > 0 && (!A || !lam || !phi || !status)))
     return set_err(SD_EINVAL, "sd_eig2: bad argument");
   if (n == 0) return SD_OK;
-  eig2_kernel<false, kReport><<<grid_for(n), kThreads, 0, s>>>(A, n, lam, phi, status, d);
+  if (aligned(lam, 16))
+    eig2_kernel<true, kReport><<<grid_for(n), kThreads, 0, s>>>(A, n, lam, phi, status, d);
+  else
+    eig2_kernel<false, kReport><<<grid_for(n), kThreads, 0, s>>>(A, n, lam, phi, status, d);
   return check_launch("eig2_kernel");
 }
 
