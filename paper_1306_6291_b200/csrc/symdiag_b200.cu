@@ -175,6 +175,73 @@ __device__ __forceinline__ sd::Sym3 load_row(const T* p) {
 constexpr int kFastRows = SD_FAST_ROWS;
 constexpr int kFastSlots = kFastRows * kFastThreads;
 
+// ---- hand-off of sparse Generic / DoubleRoot work to the compaction pass --
+// A block whose Generic (or DoubleRoot) rows would fill fewer than
+// kPassMin of its 256 queue slots leaves them to eig3_pass_kernel, which
+// gathers such rows across many tiles into full 256-row rounds: on a mixed
+// batch the long Generic path then runs on full blocks instead of 2-3 busy
+// warps per block (the rest idle until the block retires).
+#ifndef SD_PASS
+#define SD_PASS 1
+#endif
+constexpr int kPassMin = 192;
+
+// The eigenvalues of a pending row wait in its own output slots: 3 doubles
+// in lam (fp64), or split over the 24 bytes of lam + ang (fp32).
+template <typename T>
+__device__ __forceinline__ void stash_lam(T* lam, T* ang, int64_t r, const double l[3]) {
+  if (sizeof(T) == 8) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) reinterpret_cast<double*>(lam)[3 * r + k] = l[k];
+  } else {
+    uint32_t w[6];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(l[k]);
+      w[2 * k] = (uint32_t)b;
+      w[2 * k + 1] = (uint32_t)(b >> 32);
+    }
+    uint32_t* pl = reinterpret_cast<uint32_t*>(lam) + 3 * r;
+    uint32_t* pa = reinterpret_cast<uint32_t*>(ang) + 3 * r;
+    pl[0] = w[0], pl[1] = w[1], pl[2] = w[2];
+    pa[0] = w[3], pa[1] = w[4], pa[2] = w[5];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void unstash_lam(const T* lam, const T* ang, int64_t r, double l[3]) {
+  if (sizeof(T) == 8) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) l[k] = reinterpret_cast<const double*>(lam)[3 * r + k];
+  } else {
+    const uint32_t* pl = reinterpret_cast<const uint32_t*>(lam) + 3 * r;
+    const uint32_t* pa = reinterpret_cast<const uint32_t*>(ang) + 3 * r;
+    const uint32_t w[6] = {pl[0], pl[1], pl[2], pa[0], pa[1], pa[2]};
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      l[k] = __longlong_as_double((long long)(((unsigned long long)w[2 * k + 1] << 32) | w[2 * k]));
+  }
+}
+
+// Store a fast-path outcome of row r (phase B and the compaction pass).
+template <typename T>
+__device__ __forceinline__ void store_fast(T* lam, T* ang, uint8_t* status, int64_t r, int rc,
+                                          const double l[3], const double phi[3], uint8_t st) {
+  if (rc == sd::kFastDone || rc == sd::kFastPolish) {
+    // done, or closed form written with the polish pending (fp32: the
+    // polish pass recomputes the fp64 closed form itself)
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      lam[3 * r + k] = (T)l[k];
+      ang[3 * r + k] = (T)phi[k];
+    }
+  } else if (rc == sd::kFastError) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) lam[3 * r + k] = ang[3 * r + k] = (T)sd::qnan();
+  }
+  status[r] = st;  // branch code, kPolish*, or kDeferred with its reason
+}
+
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     eig3_fast_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
@@ -257,11 +324,19 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
   }
   __syncthreads();
   const int ng = qgen, nd = qdbl;
+  const bool pass_gen = SD_PASS && ng < kPassMin * kFastRows;
+  const bool pass_dbl = SD_PASS && nd < kPassMin * kFastRows;
 #pragma unroll 1
   for (int slot = tid; slot < kFastSlots; slot += kFastThreads) {
     const bool is_gen = slot < ng;
     if (!is_gen && slot < kFastSlots - nd) continue;
     const int64_t r = blk0 + qrow[slot];
+    if (is_gen ? pass_gen : pass_dbl) {
+      const double gl[3] = {ql[0][slot], ql[1][slot], ql[2][slot]};
+      stash_lam<T>(lam, ang, r, gl);
+      status[r] = is_gen ? sd::kGenPending : sd::kDblPending;
+      continue;
+    }
     sd::Sym3 g;
     if (kStoreA) {
       g.a11 = qa[0][slot];
@@ -279,19 +354,125 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     const double scale = sd::fast_scale(g);
     const int rc = is_gen ? sd::fast_generic(g, scale, gl, phi, st)
                           : sd::fast_double(g, scale, gl, phi, st);
-    if (rc == sd::kFastDone || rc == sd::kFastPolish) {
-      // done, or closed form written with the polish pending (fp32: the
-      // polish pass recomputes the fp64 closed form itself)
+    store_fast<T>(lam, ang, status, r, rc, gl, phi, st);
+  }
+}
+
+// ---- compaction pass for the rows handed off above -----------------------
+// Persistent, 256 threads: strides over 2048-row tiles of status bytes,
+// queues kGenPending rows from the front and kDblPending rows from the back
+// of one shared array, and runs a queue in rounds of 256 rows (one per
+// thread, branch-homogeneous) whenever it holds a full round.
+constexpr int kPassThreads = 256;
+constexpr int kPassTile = 2048;
+constexpr int kPassCap = kPassTile + 2 * kPassThreads;
+
+template <typename T, bool kGen>
+__device__ __forceinline__ void pass_row(const T* __restrict__ A, T* __restrict__ lam,
+                                         T* __restrict__ ang, uint8_t* __restrict__ status,
+                                         int64_t r) {
+  const sd::Sym3 a = load_row(A + 6 * r);
+  double l[3], phi[3];
+  unstash_lam<T>(lam, ang, r, l);
+  uint8_t st = 0;
+  const double scale = sd::fast_scale(a);
+  const int rc = kGen ? sd::fast_generic(a, scale, l, phi, st) : sd::fast_double(a, scale, l, phi, st);
+  store_fast<T>(lam, ang, status, r, rc, l, phi, st);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
+    eig3_pass_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
+                     T* __restrict__ ang, uint8_t* __restrict__ status, int vec) {
+  __shared__ int64_t q[kPassCap];  // generic rows from the front, double roots from the back
+  __shared__ int cg, cd;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) cg = cd = 0;
+  __syncthreads();
+  const int64_t ntiles = (n + kPassTile - 1) / kPassTile;
+  for (int64_t tile = blockIdx.x;; tile += gridDim.x) {
+    const bool live = tile < ntiles;
+    if (live) {
+      // 8 status bytes per thread: one 8-byte load when the tile is full and aligned
+      const int64_t r0 = tile * kPassTile + (int64_t)tid * 8;
+      unsigned mg = 0, md = 0;
+      if (vec && tile * kPassTile + kPassTile <= n) {
+        const uint2 w = __ldcg(reinterpret_cast<const uint2*>(status + r0));
+        const unsigned words[2] = {w.x, w.y};
 #pragma unroll
-      for (int k = 0; k < 3; k++) {
-        lam[3 * r + k] = (T)gl[k];
-        ang[3 * r + k] = (T)phi[k];
+        for (int j = 0; j < 2; j++) {
+          const unsigned eg = __vcmpeq4(words[j], 0x01010101u * sd::kGenPending);
+          const unsigned ed = __vcmpeq4(words[j], 0x01010101u * sd::kDblPending);
+          if (!(eg | ed)) continue;
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            mg |= ((eg >> (8 * k)) & 1u) << (4 * j + k);
+            md |= ((ed >> (8 * k)) & 1u) << (4 * j + k);
+          }
+        }
+      } else {
+        for (int k = 0; k < 8; k++) {
+          if (r0 + k >= n) break;
+          const unsigned b = status[r0 + k];
+          mg |= (unsigned)(b == sd::kGenPending) << k;
+          md |= (unsigned)(b == sd::kDblPending) << k;
+        }
       }
-    } else if (rc == sd::kFastError) {
+      // most tiles of a batch without hand-offs hold no pending row at all
+      if (!__syncthreads_or((mg | md) != 0u)) goto round;
+      // warp-inclusive scans, one shared atomic per warp and queue
+      int ig = __popc(mg), id = __popc(md);
+      const int mine_g = ig, mine_d = id;
 #pragma unroll
-      for (int k = 0; k < 3; k++) lam[3 * r + k] = ang[3 * r + k] = (T)sd::qnan();
+      for (int o = 1; o < 32; o <<= 1) {
+        const int vg = __shfl_up_sync(0xffffffffu, ig, o);
+        const int vd = __shfl_up_sync(0xffffffffu, id, o);
+        if (lane >= o) {
+          ig += vg;
+          id += vd;
+        }
+      }
+      int bg = 0, bd = 0;
+      if (lane == 31) {
+        if (ig) bg = atomicAdd(&cg, ig);
+        if (id) bd = atomicAdd(&cd, id);
+      }
+      bg = __shfl_sync(0xffffffffu, bg, 31) + ig - mine_g;
+      bd = __shfl_sync(0xffffffffu, bd, 31) + id - mine_d;
+      while (mg) {
+        const int k = __ffs(mg) - 1;
+        mg &= mg - 1;
+        q[bg++] = r0 + k;
+      }
+      while (md) {
+        const int k = __ffs(md) - 1;
+        md &= md - 1;
+        q[kPassCap - 1 - bd++] = r0 + k;
+      }
+      __syncthreads();
     }
-    status[r] = st;  // branch code, kPolish*, or kDeferred with its reason
+  round:
+    const int ng = cg, nd = cd;
+    const bool last = !live || tile + gridDim.x >= ntiles;
+    // run every full round; on the last tile also the partial remainder
+    const int run_g = last ? ng : ng - ng % kPassThreads;
+    const int run_d = last ? nd : nd - nd % kPassThreads;
+    if (run_g | run_d) {  // block-uniform
+      for (int k = tid; k < run_g; k += kPassThreads) pass_row<T, true>(A, lam, ang, status, q[k]);
+      for (int k = tid; k < run_d; k += kPassThreads)
+        pass_row<T, false>(A, lam, ang, status, q[kPassCap - 1 - k]);
+      __syncthreads();
+      // keep the remainders (< one round each) at the two ends of the queue
+      if (tid < ng - run_g) q[tid] = q[run_g + tid];
+      if (tid < nd - run_d) q[kPassCap - 1 - tid] = q[kPassCap - 1 - run_d - tid];
+      __syncthreads();
+      if (tid == 0) {
+        cg = ng - run_g;
+        cd = nd - run_d;
+      }
+      __syncthreads();
+    }
+    if (last) break;
   }
 }
 
@@ -388,7 +569,17 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
 template <bool kPolish>
 __device__ __forceinline__ bool fix_mine(unsigned byte) {
   const unsigned code = byte & SD_CODE_MASK;
-  return kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST) : (code == sd::kDeferred);
+  return kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST)
+                 : (code == sd::kDeferred && byte != sd::kGenPending && byte != sd::kDblPending);
+}
+
+// nonzero if any of the four status bytes in w belongs to this pass
+template <bool kPolish>
+__device__ __forceinline__ unsigned fix_mine4(unsigned w) {
+  const unsigned c = w & 0x0F0F0F0Fu;
+  if (kPolish) return __vcmpgeu4(c, 0x05050505u) & __vcmpleu4(c, 0x07070707u);
+  return __vcmpeq4(c, 0x04040404u) & ~__vcmpeq4(w, 0x01010101u * sd::kGenPending) &
+         ~__vcmpeq4(w, 0x01010101u * sd::kDblPending);
 }
 
 template <typename T, bool kPolish>
@@ -411,13 +602,20 @@ __global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_ker
     if (vec && tile * kFixTile + kFixTile <= n) {
       const uint4 w = __ldcg(reinterpret_cast<const uint4*>(status + r0));
       const unsigned words[4] = {w.x, w.y, w.z, w.w};
+      // four bytes per SIMD compare; the per-byte loop only on words that hit
 #pragma unroll
-      for (int q = 0; q < 16; q++)
-        if (fix_mine<kPolish>((words[q >> 2] >> (8 * (q & 3))) & 0xffu)) mask |= 1u << q;
+      for (int j = 0; j < 4; j++) {
+        if (!fix_mine4<kPolish>(words[j])) continue;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (fix_mine<kPolish>((words[j] >> (8 * q)) & 0xffu)) mask |= 1u << (4 * j + q);
+      }
     } else {
       for (int q = 0; q < 16; q++)
         if (r0 + q < n && fix_mine<kPolish>(status[r0 + q])) mask |= 1u << q;
     }
+    // tiles with no row for this pass skip the queue logic (one barrier)
+    if (!__syncthreads_or(mask != 0u)) continue;
     // warp-inclusive scan of the per-thread counts, one shared atomic per warp
     const int mine = __popc(mask);
     int incl = mine;
@@ -455,6 +653,16 @@ int fixup_grid(int64_t n) {
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
   const int64_t g = (int64_t)nsm * SD_FIX_MIN_BLOCKS;
   return (int)(ntiles < g ? ntiles : g);
+}
+
+unsigned pass_grid(int64_t n) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (nsm <= 0) nsm = 148;
+  const int64_t ntiles = (n + kPassTile - 1) / kPassTile;
+  const int64_t g = (int64_t)nsm * SD_FAST_MIN_BLOCKS;
+  return (unsigned)(ntiles < g ? ntiles : g);
 }
 
 // ---- fused diagonalize2 -----------------------------------------------------
@@ -789,6 +997,12 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   if (rc != SD_OK) return rc;
   const unsigned g2 = (unsigned)fixup_grid(n);
   const int vec = aligned(status, 16) ? 1 : 0;
+  if (SD_PASS) {
+    eig3_pass_kernel<T><<<pass_grid(n), kPassThreads, 0, s>>>(A, n, lam, ang, status,
+                                                               aligned(status, 8) ? 1 : 0);
+    rc = check_launch("eig3_pass_kernel");
+    if (rc != SD_OK) return rc;
+  }
   eig3_fixup_kernel<T, true><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status, vec);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;

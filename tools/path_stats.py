@@ -23,8 +23,8 @@ sys.path.insert(0, str(ROOT))
 REASONS = {1: "nonfinite_or_huge", 2: "p_negative", 3: "triple_near_gate", 4: "acos_slack",
            5: "eigen_gap", 6: "vw_excursion", 7: "f_norm_zero", 8: "zero_g_or_z",
            9: "selection_margin", 10: "phi1_route_range", 11: "residual_near_gate",
-           12: "not_double_root", 13: "double_s_excursion", 14: "double_f_norm_zero",
-           15: "double_zero_g_or_z", 0: "unspecified"}
+           12: "not_double_root", 13: "double_pending_pass", 14: "double_f_norm_zero",
+           15: "double_zero_g_or_z", 0: "generic_pending_pass"}
 
 
 def main():
