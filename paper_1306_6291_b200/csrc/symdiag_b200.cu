@@ -184,7 +184,16 @@ constexpr int kFastSlots = kFastRows * kFastThreads;
 #ifndef SD_PASS
 #define SD_PASS 1
 #endif
-constexpr int kPassMin = 192;
+#ifndef SD_PASS_MIN
+#define SD_PASS_MIN 192
+#endif
+// DoubleRoot rows are cheaper than Generic ones: a block keeps them unless
+// there are very few (measured: c3 -3.7%, c2/c4 +-0.2%,
+// profiles/r1_variants19_pass_thresholds.jsonl)
+#ifndef SD_PASS_MIN_DBL
+#define SD_PASS_MIN_DBL 16
+#endif
+constexpr int kPassMin = SD_PASS_MIN, kPassMinDbl = SD_PASS_MIN_DBL;
 
 // The eigenvalues of a pending row wait in its own output slots: 3 doubles
 // in lam (fp64), or split over the 24 bytes of lam + ang (fp32).
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
   __syncthreads();
   const int ng = qgen, nd = qdbl;
   const bool pass_gen = SD_PASS && ng < kPassMin * kFastRows;
-  const bool pass_dbl = SD_PASS && nd < kPassMin * kFastRows;
+  const bool pass_dbl = SD_PASS && nd < kPassMinDbl * kFastRows;
 #pragma unroll 1
   for (int slot = tid; slot < kFastSlots; slot += kFastThreads) {
     const bool is_gen = slot < ng;
