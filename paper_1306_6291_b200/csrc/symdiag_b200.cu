@@ -184,6 +184,9 @@ constexpr int kFastSlots = kFastRows * kFastThreads;
 #ifndef SD_PASS
 #define SD_PASS 1
 #endif
+#ifndef SD_PDL
+#define SD_PDL 1
+#endif
 #ifndef SD_PASS_MIN
 #define SD_PASS_MIN 192
 #endif
@@ -389,6 +392,16 @@ __device__ __forceinline__ void pass_row(const T* __restrict__ A, T* __restrict_
   store_fast<T>(lam, ang, status, r, rc, l, phi, st);
 }
 
+// Programmatic dependent launch: the passes after the fast kernel are
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization, so their
+// launch overlaps the previous kernel's tail; each waits here until the
+// previous grid has completed and its writes are visible.
+__device__ __forceinline__ void wait_prior_grid() {
+#if SD_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
     eig3_pass_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
@@ -396,6 +409,7 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
   __shared__ int64_t q[kPassCap];  // generic rows from the front, double roots from the back
   __shared__ int cg, cd;
   const int tid = threadIdx.x, lane = tid & 31;
+  wait_prior_grid();
   if (tid == 0) cg = cd = 0;
   __syncthreads();
   const int64_t ntiles = (n + kPassTile - 1) / kPassTile;
@@ -600,6 +614,7 @@ __global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_ker
   __shared__ int64_t queue[kFixQueue];
   __shared__ int cnt;
   const int tid = threadIdx.x, lane = tid & 31;
+  wait_prior_grid();
   if (tid == 0) cnt = 0;
   __syncthreads();
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
@@ -662,6 +677,27 @@ int fixup_grid(int64_t n) {
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
   const int64_t g = (int64_t)nsm * SD_FIX_MIN_BLOCKS;
   return (int)(ntiles < g ? ntiles : g);
+}
+
+// launch a pass that starts with wait_prior_grid(): with SD_PDL as a
+// programmatic dependent launch, else an ordinary stream-ordered launch
+template <typename... KArgs, typename... Args>
+void launch_after(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
+                  Args... args) {
+#if SD_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+#else
+  kernel<<<grid, block, 0, s>>>(static_cast<KArgs>(args)...);
+#endif
 }
 
 unsigned pass_grid(int64_t n) {
@@ -1007,15 +1043,15 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   const unsigned g2 = (unsigned)fixup_grid(n);
   const int vec = aligned(status, 16) ? 1 : 0;
   if (SD_PASS) {
-    eig3_pass_kernel<T><<<pass_grid(n), kPassThreads, 0, s>>>(A, n, lam, ang, status,
-                                                               aligned(status, 8) ? 1 : 0);
+    launch_after(eig3_pass_kernel<T>, pass_grid(n), kPassThreads, s, A, n, lam, ang, status,
+                 aligned(status, 8) ? 1 : 0);
     rc = check_launch("eig3_pass_kernel");
     if (rc != SD_OK) return rc;
   }
-  eig3_fixup_kernel<T, true><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status, vec);
+  launch_after(eig3_fixup_kernel<T, true>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;
-  eig3_fixup_kernel<T, false><<<g2, kFixThreads, 0, s>>>(A, n, lam, ang, status, vec);
+  launch_after(eig3_fixup_kernel<T, false>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
   return check_launch("eig3_literal_kernel");
 }
 
