@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
 // of one shared array, and runs a queue in rounds of 256 rows (one per
 // thread, branch-homogeneous) whenever it holds a full round.
 constexpr int kPassThreads = 256;
-constexpr int kPassTile = 2048;
+constexpr int kPassTile = 4096;  // 16 status bytes per thread
 constexpr int kPassCap = kPassTile + 2 * kPassThreads;
 
 template <typename T, bool kGen>
@@ -406,7 +406,9 @@ template <typename T>
 __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
     eig3_pass_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
                      T* __restrict__ ang, uint8_t* __restrict__ status, int vec) {
-  __shared__ int64_t q[kPassCap];  // generic rows from the front, double roots from the back
+  // generic rows from the front, double roots from the back (row < 2^32:
+  // launch_eig3_fast splits larger batches)
+  __shared__ uint32_t q[kPassCap];
   __shared__ int cg, cd;
   const int tid = threadIdx.x, lane = tid & 31;
   wait_prior_grid();
@@ -416,14 +418,14 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
   for (int64_t tile = blockIdx.x;; tile += gridDim.x) {
     const bool live = tile < ntiles;
     if (live) {
-      // 8 status bytes per thread: one 8-byte load when the tile is full and aligned
-      const int64_t r0 = tile * kPassTile + (int64_t)tid * 8;
+      // 16 status bytes per thread: one 16-byte load when the tile is full and aligned
+      const int64_t r0 = tile * kPassTile + (int64_t)tid * 16;
       unsigned mg = 0, md = 0;
       if (vec && tile * kPassTile + kPassTile <= n) {
-        const uint2 w = __ldcg(reinterpret_cast<const uint2*>(status + r0));
-        const unsigned words[2] = {w.x, w.y};
+        const uint4 w = __ldcg(reinterpret_cast<const uint4*>(status + r0));
+        const unsigned words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int j = 0; j < 2; j++) {
+        for (int j = 0; j < 4; j++) {
           const unsigned eg = __vcmpeq4(words[j], 0x01010101u * sd::kGenPending);
           const unsigned ed = __vcmpeq4(words[j], 0x01010101u * sd::kDblPending);
           if (!(eg | ed)) continue;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
           }
         }
       } else {
-        for (int k = 0; k < 8; k++) {
+        for (int k = 0; k < 16; k++) {
           if (r0 + k >= n) break;
           const unsigned b = status[r0 + k];
           mg |= (unsigned)(b == sd::kGenPending) << k;
@@ -465,12 +467,12 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
       while (mg) {
         const int k = __ffs(mg) - 1;
         mg &= mg - 1;
-        q[bg++] = r0 + k;
+        q[bg++] = (uint32_t)(r0 + k);
       }
       while (md) {
         const int k = __ffs(md) - 1;
         md &= md - 1;
-        q[kPassCap - 1 - bd++] = r0 + k;
+        q[kPassCap - 1 - bd++] = (uint32_t)(r0 + k);
       }
       __syncthreads();
     }
@@ -1033,6 +1035,17 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   if (n < 0 || (n > 0 && (!A || !lam || !ang || !status)))
     return set_err(SD_EINVAL, "sd_eig3: bad argument");
   if (n == 0) return SD_OK;
+  // the compaction pass queues 32-bit row indices: segment larger batches
+  // (only reachable with > 200 GB of fp32 rows, i.e. not on one B200)
+  constexpr int64_t kSeg = (int64_t)1 << 31;
+  if (n > kSeg) {
+    for (int64_t r0 = 0; r0 < n; r0 += kSeg) {
+      const int64_t m = (n - r0) < kSeg ? (n - r0) : kSeg;
+      const int rc = launch_eig3_fast<T>(A + 6 * r0, m, lam + 3 * r0, ang + 3 * r0, status + r0, s);
+      if (rc != SD_OK) return rc;
+    }
+    return SD_OK;
+  }
   const unsigned g1 = (unsigned)((n + kFastSlots - 1) / kFastSlots);
   if (aligned(A, 2 * sizeof(T)))
     eig3_fast_kernel<T, true><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
@@ -1044,7 +1057,7 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   const int vec = aligned(status, 16) ? 1 : 0;
   if (SD_PASS) {
     launch_after(eig3_pass_kernel<T>, pass_grid(n), kPassThreads, s, A, n, lam, ang, status,
-                 aligned(status, 8) ? 1 : 0);
+                 vec);
     rc = check_launch("eig3_pass_kernel");
     if (rc != SD_OK) return rc;
   }
