@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
 // once a full block's worth has accumulated.  Dense warps, no tail of
 // one-row blocks, no global workspace.  Two separate launches keep each
 // kernel's code small (the literal solver is ~13k SASS instructions).
-constexpr int kFixTile = 2048;
+constexpr int kFixTile = 4096;  // 32 status bytes per thread
 #ifndef SD_FIX_MIN_BLOCKS
 #define SD_FIX_MIN_BLOCKS 4
 #endif
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_ker
                                                                  T* __restrict__ ang,
                                                                  uint8_t* __restrict__ status,
                                                                  int vec) {
-  __shared__ int64_t queue[kFixQueue];
+  __shared__ uint32_t queue[kFixQueue];  // rows < 2^32: launch_eig3_fast segments larger batches
   __shared__ int cnt;
   const int tid = threadIdx.x, lane = tid & 31;
   wait_prior_grid();
@@ -621,23 +621,24 @@ __global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_ker
   __syncthreads();
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    // each thread owns kFixTile / kFixThreads = 16 consecutive status bytes:
-    // one 16-byte load when the tile is complete and aligned
-    const int64_t r0 = tile * kFixTile + (int64_t)tid * 16;
+    // each thread owns kFixTile / kFixThreads = 32 consecutive status bytes:
+    // two 16-byte loads when the tile is complete and aligned
+    const int64_t r0 = tile * kFixTile + (int64_t)tid * 32;
     unsigned mask = 0;
     if (vec && tile * kFixTile + kFixTile <= n) {
-      const uint4 w = __ldcg(reinterpret_cast<const uint4*>(status + r0));
-      const unsigned words[4] = {w.x, w.y, w.z, w.w};
+      const uint4 w0 = __ldcg(reinterpret_cast<const uint4*>(status + r0));
+      const uint4 w1 = __ldcg(reinterpret_cast<const uint4*>(status + r0 + 16));
+      const unsigned words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
       // four bytes per SIMD compare; the per-byte loop only on words that hit
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < 8; j++) {
         if (!fix_mine4<kPolish>(words[j])) continue;
 #pragma unroll
         for (int q = 0; q < 4; q++)
           if (fix_mine<kPolish>((words[j] >> (8 * q)) & 0xffu)) mask |= 1u << (4 * j + q);
       }
     } else {
-      for (int q = 0; q < 16; q++)
+      for (int q = 0; q < 32; q++)
         if (r0 + q < n && fix_mine<kPolish>(status[r0 + q])) mask |= 1u << q;
     }
     // tiles with no row for this pass skip the queue logic (one barrier)
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_ker
     while (mask) {
       const int q = __ffs(mask) - 1;
       mask &= mask - 1;
-      queue[base++] = r0 + q;
+      queue[base++] = (uint32_t)(r0 + q);
     }
     __syncthreads();
     const int c = cnt;
