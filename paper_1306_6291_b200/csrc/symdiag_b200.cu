@@ -376,7 +376,11 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
 // of one shared array, and runs a queue in rounds of 256 rows (one per
 // thread, branch-homogeneous) whenever it holds a full round.
 constexpr int kPassThreads = 256;
-constexpr int kPassTile = 4096;  // 16 status bytes per thread
+#ifndef SD_PASS_BYTES
+#define SD_PASS_BYTES 16  // status bytes per thread and tile (16 or 32)
+#endif
+constexpr int kPassBytes = SD_PASS_BYTES;
+constexpr int kPassTile = kPassThreads * kPassBytes;
 constexpr int kPassCap = kPassTile + 2 * kPassThreads;
 
 template <typename T, bool kGen>
@@ -418,14 +422,18 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
   for (int64_t tile = blockIdx.x;; tile += gridDim.x) {
     const bool live = tile < ntiles;
     if (live) {
-      // 16 status bytes per thread: one 16-byte load when the tile is full and aligned
-      const int64_t r0 = tile * kPassTile + (int64_t)tid * 16;
+      // kPassBytes status bytes per thread: 16-byte loads when the tile is full and aligned
+      const int64_t r0 = tile * kPassTile + (int64_t)tid * kPassBytes;
       unsigned mg = 0, md = 0;
       if (vec && tile * kPassTile + kPassTile <= n) {
-        const uint4 w = __ldcg(reinterpret_cast<const uint4*>(status + r0));
-        const unsigned words[4] = {w.x, w.y, w.z, w.w};
+        unsigned words[kPassBytes / 4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
+        for (int v = 0; v < kPassBytes / 16; v++) {
+          const uint4 w = __ldcg(reinterpret_cast<const uint4*>(status + r0) + v);
+          words[4 * v] = w.x, words[4 * v + 1] = w.y, words[4 * v + 2] = w.z, words[4 * v + 3] = w.w;
+        }
+#pragma unroll
+        for (int j = 0; j < kPassBytes / 4; j++) {
           const unsigned eg = __vcmpeq4(words[j], 0x01010101u * sd::kGenPending);
           const unsigned ed = __vcmpeq4(words[j], 0x01010101u * sd::kDblPending);
           if (!(eg | ed)) continue;
@@ -436,7 +444,7 @@ __global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
           }
         }
       } else {
-        for (int k = 0; k < 16; k++) {
+        for (int k = 0; k < kPassBytes; k++) {
           if (r0 + k >= n) break;
           const unsigned b = status[r0 + k];
           mg |= (unsigned)(b == sd::kGenPending) << k;
