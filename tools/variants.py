@@ -32,6 +32,9 @@ VARIANTS = {
 def build():
     from paper_1306_6291_b200 import build_ext
     OUT.mkdir(parents=True, exist_ok=True)
+    for old in OUT.glob("lib_*.so"):  # stale variants would bloat the gpurun snapshot
+        if old.stem[4:] not in VARIANTS:
+            old.unlink()
     from concurrent.futures import ThreadPoolExecutor
 
     def one(item):
