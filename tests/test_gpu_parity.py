@@ -604,3 +604,21 @@ def test_unaligned_outputs_take_the_scalar_scan_paths():
     same = lambda x, y: bool(((x == y) | (torch.isnan(x) & torch.isnan(y))).all())  # noqa: E731
     assert torch.equal(st, ref.status)
     assert same(lam, ref.lam) and same(ang, ref.ang)
+
+
+def test_fp32_mixed_batch_through_the_compaction_pass():
+    """fp32 storage on the degenerate-stress mix: most Generic rows are handed
+    to the compaction pass, their fp64 eigenvalues stashed across the fp32
+    lam + ang slots meanwhile.  Same status as the oracle's fp32 entry,
+    eigenvalues within 1e-5 normwise."""
+    A32 = workloads.generate("c3", 1 << 17).astype(np.float32)
+    ref = O.eig3_f32(A32, nthreads=O.default_threads())
+    got = gpu3(A32, dtype=torch.float32)
+    code_mis = ((ref["status"] ^ got["status"]) & 0x0F) != 0
+    assert code_mis.sum() <= 2
+    ok = ~code_mis & ((ref["status"] & 0x0F) < 8)
+    lr = ref["lam"][ok].astype(np.float64)
+    norm = np.maximum(1.0, np.abs(lr).max(axis=1, keepdims=True))
+    assert (np.abs(got["lam"][ok] - lr) / norm).max() <= 1e-5
+    gen = ok & ((ref["status"] & 0x0F) == 0) & (((ref["status"] | got["status"]) & 0x80) == 0)
+    assert wrapped_diff(got["ang"][gen], ref["ang"][gen]).max() <= 1e-5
