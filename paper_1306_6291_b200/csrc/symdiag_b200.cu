@@ -722,39 +722,260 @@ unsigned pass_grid(int64_t n) {
 }
 
 // ---- fused diagonalize2 -----------------------------------------------------
+// Three kernel shapes (SD_EIG2_MODE, measured by tools/eig2_variants.py):
+//  0  tile: kEig2Rows rows per thread, all loads issued before any arithmetic;
+//  1  stream: persistent grid-stride loop, the next row's loads in flight
+//     while the current row computes;
+//  2  bulk: persistent, each block streams 256-row tiles (6 KB) into a
+//     kEig2Stages-deep shared-memory ring with cp.async.bulk (TMA bulk copy,
+//     mbarrier completion), one elected thread issuing; the rows are read from
+//     shared memory (stride 24 B: conflict-free per half warp).
+// Every load / store instruction of a warp covers one contiguous span; (l1, l2)
+// leaves as one 16-byte store per lane when lam is 16-byte aligned (kVec).
+#ifndef SD_EIG2_MODE
+#define SD_EIG2_MODE 0
+#endif
+#ifndef SD_EIG2_ROWS
+#define SD_EIG2_ROWS 2
+#endif
+#ifndef SD_EIG2_THREADS
+#define SD_EIG2_THREADS 128
+#endif
+#ifndef SD_EIG2_STAGES
+#define SD_EIG2_STAGES 3
+#endif
+#ifndef SD_EIG2_BLOCKS_PER_SM
+#define SD_EIG2_BLOCKS_PER_SM 4
+#endif
+constexpr int kEig2Rows = SD_EIG2_ROWS;
+constexpr int kEig2Threads = SD_EIG2_THREADS;
+constexpr int kEig2Stages = SD_EIG2_STAGES;
+
 template <bool kVec, bool kReport>
-__global__ void __launch_bounds__(kThreads) eig2_kernel(const double* __restrict__ A, int64_t n,
-                                                        double* __restrict__ lam,
-                                                        double* __restrict__ phi,
-                                                        uint8_t* __restrict__ status,
-                                                        double* __restrict__ dmat) {
-  // One row per thread, no shared-memory staging: the warp's three 8-byte
-  // loads per row cover the same 768 contiguous bytes (L1 serves the second
-  // and third), and (l1, l2) leaves as one 16-byte store per lane, a
-  // contiguous 512-byte warp store when lam is 16-byte aligned (kVec).
-  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (i >= n) return;
-  const double* p = A + 3 * i;
-  double l1, l2, ph;
-  const uint8_t st = sd::diagonalize2(__ldg(p), __ldg(p + 1), __ldg(p + 2), l1, l2, ph);
+__device__ __forceinline__ void eig2_store(int64_t i, bool ok, double a11, double a12, double a22,
+                                           double l1, double l2, double ph,
+                                           double* __restrict__ lam, double* __restrict__ phi,
+                                           uint8_t* __restrict__ status,
+                                           double* __restrict__ dmat) {
+  uint8_t st = SD_CODE_GENERIC;
+  if (!ok) {
+    double s1, s2, sp;  // address-taken by the out-of-line call: kept off the fast path
+    st = sd::diagonalize2_literal(a11, a12, a22, s1, s2, sp);
+    l1 = s1;
+    l2 = s2;
+    ph = sp;
+  }
   if (kVec) {
     reinterpret_cast<double2*>(lam)[i] = make_double2(l1, l2);
   } else {
     lam[2 * i] = l1;
     lam[2 * i + 1] = l2;
   }
-  {
-    phi[i] = ph;
-    status[i] = st;
-    if (kReport && dmat) {
-      double c = sd::qnan(), s = sd::qnan();
-      if (st == SD_CODE_GENERIC) sincos(ph, &s, &c);
-      dmat[4 * i + 0] = c;
-      dmat[4 * i + 1] = -s;
-      dmat[4 * i + 2] = s;
-      dmat[4 * i + 3] = c;
+  phi[i] = ph;
+  status[i] = st;
+  if (kReport && dmat) {
+    double c = sd::qnan(), s = sd::qnan();
+    if (st == SD_CODE_GENERIC) sincos(ph, &s, &c);
+    dmat[4 * i + 0] = c;
+    dmat[4 * i + 1] = -s;
+    dmat[4 * i + 2] = s;
+    dmat[4 * i + 3] = c;
+  }
+}
+
+template <bool kVec, bool kReport>
+__device__ __forceinline__ void eig2_row(double a11, double a12, double a22, int64_t i,
+                                         double* __restrict__ lam, double* __restrict__ phi,
+                                         uint8_t* __restrict__ status, double* __restrict__ dmat) {
+  double l1, l2, ph;
+  const bool ok = !SD_EIG2_LITERAL && sd::diagonalize2_fast(a11, a12, a22, l1, l2, ph);
+  eig2_store<kVec, kReport>(i, ok, a11, a12, a22, l1, l2, ph, lam, phi, status, dmat);
+}
+
+// R rows of one thread: the branch-free fast paths of all R rows first (R
+// independent dependency chains the scheduler interleaves), then fix-ups and
+// stores; rows at index >= n are skipped.
+template <int R, bool kVec, bool kReport>
+__device__ __forceinline__ void eig2_rows(const double (&a)[R][3], int64_t base, int64_t n,
+                                          double* __restrict__ lam, double* __restrict__ phi,
+                                          uint8_t* __restrict__ status,
+                                          double* __restrict__ dmat) {
+  double l1[R], l2[R], ph[R];
+  bool ok[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    ok[k] = !SD_EIG2_LITERAL && sd::diagonalize2_fast(a[k][0], a[k][1], a[k][2], l1[k], l2[k], ph[k]);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int64_t i = base + (int64_t)k * kEig2Threads;
+    if (i < n)
+      eig2_store<kVec, kReport>(i, ok[k], a[k][0], a[k][1], a[k][2], l1[k], l2[k], ph[k], lam,
+                                phi, status, dmat);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void eig2_load(const double* __restrict__ A, int64_t base, int64_t n,
+                                          double (&a)[R][3]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int64_t i = base + (int64_t)k * kEig2Threads;
+    if (i < n) {
+      a[k][0] = __ldg(A + 3 * i);
+      a[k][1] = __ldg(A + 3 * i + 1);
+      a[k][2] = __ldg(A + 3 * i + 2);
+    } else {
+      a[k][0] = a[k][1] = a[k][2] = 0.0;
     }
   }
+}
+
+template <bool kVec, bool kReport>
+__global__ void __launch_bounds__(kEig2Threads) eig2_kernel(const double* __restrict__ A, int64_t n,
+                                                            double* __restrict__ lam,
+                                                            double* __restrict__ phi,
+                                                            uint8_t* __restrict__ status,
+                                                            double* __restrict__ dmat) {
+  const int64_t base = (int64_t)blockIdx.x * (kEig2Threads * kEig2Rows) + threadIdx.x;
+  double a[kEig2Rows][3];
+  eig2_load<kEig2Rows>(A, base, n, a);
+  eig2_rows<kEig2Rows, kVec, kReport>(a, base, n, lam, phi, status, dmat);
+}
+
+#ifndef SD_EIG2_PREFETCH
+#define SD_EIG2_PREFETCH 1
+#endif
+// persistent grid-stride loop over groups of kEig2Rows rows per thread; with
+// SD_EIG2_PREFETCH the next group's loads are in flight while this group
+// computes
+template <bool kVec, bool kReport>
+__global__ void __launch_bounds__(kEig2Threads) eig2_stream_kernel(
+    const double* __restrict__ A, int64_t n, double* __restrict__ lam, double* __restrict__ phi,
+    uint8_t* __restrict__ status, double* __restrict__ dmat) {
+  const int64_t stride = (int64_t)gridDim.x * kEig2Threads * kEig2Rows;
+  int64_t base = (int64_t)blockIdx.x * kEig2Threads * kEig2Rows + threadIdx.x;
+  if (base >= n) return;
+  double c[kEig2Rows][3];
+  eig2_load<kEig2Rows>(A, base, n, c);
+  for (;;) {
+    const int64_t nb = base + stride;
+    if (SD_EIG2_PREFETCH) {
+      double nx[kEig2Rows][3];
+      eig2_load<kEig2Rows>(A, nb, n, nx);
+      eig2_rows<kEig2Rows, kVec, kReport>(c, base, n, lam, phi, status, dmat);
+#pragma unroll
+      for (int k = 0; k < kEig2Rows; ++k) {
+        c[k][0] = nx[k][0];
+        c[k][1] = nx[k][1];
+        c[k][2] = nx[k][2];
+      }
+    } else {
+      eig2_rows<kEig2Rows, kVec, kReport>(c, base, n, lam, phi, status, dmat);
+      eig2_load<kEig2Rows>(A, nb, n, c);
+    }
+    if (nb >= n) break;
+    base = nb;
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// A must be 16-byte aligned (bulk copies move 16-byte multiples from 16-byte
+// aligned addresses); a tile of 256 rows is 6144 bytes.  The last, partial
+// tile (if its byte count is not a multiple of 16) is read with plain loads.
+template <bool kVec, bool kReport>
+__global__ void __launch_bounds__(kEig2Threads) eig2_bulk_kernel(
+    const double* __restrict__ A, int64_t n, double* __restrict__ lam, double* __restrict__ phi,
+    uint8_t* __restrict__ status, double* __restrict__ dmat) {
+  constexpr int kTileRows = kEig2Threads;
+  constexpr uint32_t kTileBytes = kTileRows * 24;
+  __shared__ alignas(128) double buf[kEig2Stages][kTileRows * 3];
+  __shared__ alignas(8) uint64_t bar[kEig2Stages];
+  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
+  const int64_t first = blockIdx.x;
+  const int64_t step = gridDim.x;
+  // bytes of tile t that the bulk engine moves (0: plain loads instead)
+  auto tile_bytes = [&](int64_t t) -> uint32_t {
+    const int64_t rows = n - t * kTileRows;
+    if (rows >= kTileRows) return kTileBytes;
+    const uint32_t b = (uint32_t)rows * 24u;
+    return (b % 16u) ? 0u : b;
+  };
+  auto issue = [&](int64_t t, int st) {
+    const uint32_t bytes = tile_bytes(t);
+    if (!bytes) return;
+    const uint32_t mb = smem_u32(&bar[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(&buf[st][0])),
+        "l"(A + t * (int64_t)kTileRows * 3), "r"(bytes), "r"(mb)
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kEig2Stages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[st])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < kEig2Stages; ++st) {
+      const int64_t t = first + st * step;
+      if (t < ntiles) issue(t, st);
+    }
+  }
+  __syncthreads();
+  int k = 0;
+  for (int64_t t = first; t < ntiles; t += step, ++k) {
+    const int st = k % kEig2Stages;
+    const uint32_t parity = (uint32_t)(k / kEig2Stages) & 1u;
+    const int64_t i = t * kTileRows + threadIdx.x;
+    double a11 = 0.0, a12 = 0.0, a22 = 0.0;
+    if (tile_bytes(t)) {
+      const uint32_t mb = smem_u32(&bar[st]);
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(mb), "r"(parity)
+            : "memory");
+      }
+      if (i < n) {
+        const double* r = &buf[st][3 * threadIdx.x];
+        a11 = r[0];
+        a12 = r[1];
+        a22 = r[2];
+      }
+    } else if (i < n) {
+      a11 = __ldg(A + 3 * i);
+      a12 = __ldg(A + 3 * i + 1);
+      a22 = __ldg(A + 3 * i + 2);
+    }
+    __syncthreads();  // every row of buf[st] is in registers: refill it
+    if (threadIdx.x == 0) {
+      const int64_t tn = t + (int64_t)kEig2Stages * step;
+      if (tn < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(tn, st);
+      }
+    }
+    if (i < n) eig2_row<kVec, kReport>(a11, a12, a22, i, lam, phi, status, dmat);
+  }
+}
+
+// persistent grid: SD_EIG2_BLOCKS_PER_SM resident blocks per SM, fewer for
+// small batches
+unsigned eig2_grid_persistent(int64_t n) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (nsm <= 0) nsm = 148;
+  const int64_t per = (int64_t)kEig2Threads * (SD_EIG2_MODE == 1 ? kEig2Rows : 1);
+  const int64_t blocks = (n + per - 1) / per;
+  const int64_t g = (int64_t)nsm * SD_EIG2_BLOCKS_PER_SM;
+  return (unsigned)(blocks < g ? blocks : g);
 }
 
 // ---- stage kernels (one thread per row, plain loads) -----------------------
@@ -1083,10 +1304,27 @@ int launch_eig2(const double* A, int64_t n, double* lam, double* phi, uint8_t* s
   if (n < 0 || (n > 0 && (!A || !lam || !phi || !status)))
     return set_err(SD_EINVAL, "sd_eig2: bad argument");
   if (n == 0) return SD_OK;
-  if (aligned(lam, 16))
-    eig2_kernel<true, kReport><<<grid_for(n), kThreads, 0, s>>>(A, n, lam, phi, status, d);
-  else
-    eig2_kernel<false, kReport><<<grid_for(n), kThreads, 0, s>>>(A, n, lam, phi, status, d);
+  const bool vec = aligned(lam, 16);
+  if (SD_EIG2_MODE == 2 && aligned(A, 16)) {
+    const unsigned g = eig2_grid_persistent(n);
+    if (vec)
+      eig2_bulk_kernel<true, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+    else
+      eig2_bulk_kernel<false, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+  } else if (SD_EIG2_MODE >= 1) {
+    const unsigned g = eig2_grid_persistent(n);
+    if (vec)
+      eig2_stream_kernel<true, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+    else
+      eig2_stream_kernel<false, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+  } else {
+    const int64_t tile = (int64_t)kEig2Threads * kEig2Rows;
+    const unsigned g = (unsigned)((n + tile - 1) / tile);
+    if (vec)
+      eig2_kernel<true, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+    else
+      eig2_kernel<false, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+  }
   return check_launch("eig2_kernel");
 }
 
