@@ -82,6 +82,14 @@ __device__ __forceinline__ double pow6(Err& e, double x) {
   return r;
 }
 
+// a / b for finite non-zero b, with a == +-0 answered without the division:
+// libdevice's correctly rounded division takes its slow path whenever the
+// quotient is zero
+__device__ __forceinline__ double div_nz(double a, double b) {
+  if (a == 0.0) return (signbit(a) != signbit(b)) ? -0.0 : 0.0;
+  return a / b;
+}
+
 // math_1 rules: NaN from non-NaN -> ValueError (math domain error)
 __device__ __forceinline__ double chk(Err& e, double r, double x) {
   if (is_nan(r) && !is_nan(x)) e.raise(SD_ERR_MATH_DOMAIN);
@@ -128,7 +136,11 @@ __device__ __forceinline__ double hypot_scaled(double a, double b, double scale,
   frac1 += lo;
   frac2 += r;
   double t = csum - 1.0 + (frac1 + frac2);
-  h += t / (2.0 * h);
+  // t == 0 (common when the operands carry few significant bits, e.g. the
+  // rounding-noise off-diagonals of rotated scalar matrices): h + 0 / (2h)
+  // is h bit for bit, and skipping the division avoids libdevice's slow
+  // division path, which a zero quotient always takes
+  if (t != 0.0) h += t / (2.0 * h);
   return kMul ? h * inv : h / scale;
 }
 

@@ -205,6 +205,52 @@ def test_eig2_full_config_matches_oracle():
     assert np.abs(r.phi.cpu().numpy() - ref["phi"]).max() <= 1e-15
 
 
+def eig2_boundary_rows(seed=7):
+    """Rows on and around every gate of the fast 2x2 path (sd_eig2.cuh
+    diagonalize2_fast): the 2^500 input bound and the x**2 overflow, hypot's
+    2^-1021 operand bound and subnormals, the phi = 0 gate of eig2.py:37-39
+    (m near 1e-14 max(1, ||A||_F) at several scales), the octant boundary
+    |2 a12| = |a11 - a22|, signed zeros, and wide-range random rows."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    big = [2.0 ** 499.9, 2.0 ** 500, np.nextafter(2.0 ** 500, 0), np.nextafter(2.0 ** 500, 1e308),
+           2.0 ** 510, 1.3e154, 1.35e154, 1e300, np.inf, -np.inf, np.nan]
+    for b in big:
+        rows += [(b, 0.5, 0.25), (0.5, b, 0.25), (0.25, 0.5, b), (b, b, b), (b, -b, b / 3)]
+    tiny = [2.0 ** -1021, np.nextafter(2.0 ** -1021, 0), 2.0 ** -1022, 2.0 ** -1023, 5e-324, 0.0]
+    for t in tiny:
+        rows += [(t, 0.0, 0.0), (0.0, t, 0.0), (0.0, t / 2, 0.0), (t, t, 0.0), (3 * t, t, t),
+                 (1.0, t, 1.0), (t, 0.0, -t)]
+    for scale in (1.0, 1e3, 1e-3, 1e10, 1e-10, 3.7):
+        for d in (0.0, 0.5e-14, 0.99e-14, 1e-14, 1.01e-14, 2e-14, 2.0 ** -44, 2.0 ** -45,
+                  3e-14, 1e-13, 1e-12):
+            for off in (0.0, d, -d, d / 2):
+                a22 = scale * rng.uniform(-1, 1)
+                rows += [(a22 + scale * d, scale * off, a22), (a22, scale * off, a22 + scale * d)]
+    for v in (1.0, -1.0, 3.0, 1e-300, 1e300, 2.5e-310):
+        rows += [(v, v / 2, 0.0), (0.0, v / 2, v), (v, -v / 2, 0.0), (v, v / 2, -v), (v, 0.0, v),
+                 (v, -0.0, v), (-0.0, v, 0.0), (0.0, -0.0, -0.0), (-0.0, 0.0, 0.0)]
+    e = rng.uniform(-600, 600, (4096, 3))
+    r = rng.uniform(-1, 1, (4096, 3)) * 10.0 ** rng.uniform(-3, 3, (4096, 1)) * 2.0 ** e.round()
+    return np.vstack([np.array(rows, dtype=np.float64), r])
+
+
+def test_eig2_fast_path_boundaries_match_oracle():
+    A = eig2_boundary_rows()
+    ref = O.eig2(A, d=True)
+    r = sd.diagonalize2_batched(torch.as_tensor(A).to(DEV), with_d=True)
+    torch.cuda.synchronize()
+    st = r.status.cpu().numpy()
+    assert np.array_equal(st, ref["status"])
+    ok = st == 0
+    lam = r.lam.cpu().numpy()
+    assert np.array_equal(lam[ok], ref["lam"][ok])
+    assert np.all(np.isnan(lam[~ok]))
+    phi = r.phi.cpu().numpy()
+    assert np.abs(phi[ok] - ref["phi"][ok]).max() <= 1e-15
+    assert np.array_equal(np.signbit(phi[ok]), np.signbit(ref["phi"][ok]))
+
+
 @pytest.mark.parametrize("name", ["edge", "c3"])
 def test_stage_kernels_match_reference(name):
     g = load_golden(f"stages_{name}")

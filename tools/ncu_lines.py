@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Per-source-line hot spots of one kernel from an ncu report.
 
-    python tools/ncu_lines.py <report.ncu-rep> <kernel-regex> <mangled-name-substring> [top]
+    python tools/ncu_lines.py <report.ncu-rep> <kernel-regex> <mangled-name-substring> [top] [file:line]
 
 Joins ncu's per-SASS-address metrics (source page, SASS view) with the line
 table nvdisasm -g prints for the same cubin (extracted from the in-tree
@@ -54,6 +54,7 @@ def line_table(fun_sub: str):
 def main():
     rep, kre, fun_sub = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    dump = sys.argv[5] if len(sys.argv) > 5 else None  # print this line's SASS
     raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
                           "-k", f"regex:{kre}"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -75,6 +76,8 @@ def main():
         addr -= base
         line = table.get(addr, "?")
         a = agg[line]
+        if dump and line == dump:
+            print(f"{addr:6x} {d['Instructions Executed']:>10s} {d['Thread Instructions Executed']:>12s}  {d['Source']}")
         a[0] += float(d["Instructions Executed"] or 0)
         a[1] += float(d["Thread Instructions Executed"] or 0)
         a[2] += float(d["Warp Stall Sampling (All Samples)"] or 0)
