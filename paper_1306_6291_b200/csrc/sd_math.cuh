@@ -82,11 +82,11 @@ __device__ __forceinline__ double pow6(Err& e, double x) {
   return r;
 }
 
-// a / b for finite non-zero b, with a == +-0 answered without the division:
-// libdevice's correctly rounded division takes its slow path whenever the
-// quotient is zero
+// a / b, with a == +-0 over a non-zero, non-NaN b answered without the
+// division (the same signed zero): libdevice's correctly rounded division
+// takes its slow path whenever the quotient is zero
 __device__ __forceinline__ double div_nz(double a, double b) {
-  if (a == 0.0) return (signbit(a) != signbit(b)) ? -0.0 : 0.0;
+  if (a == 0.0 && b != 0.0 && b == b) return (signbit(a) != signbit(b)) ? -0.0 : 0.0;
   return a / b;
 }
 
