@@ -747,6 +747,9 @@ unsigned pass_grid(int64_t n) {
 #ifndef SD_EIG2_BLOCKS_PER_SM
 #define SD_EIG2_BLOCKS_PER_SM 4
 #endif
+#ifndef SD_EIG2_MIN_BLOCKS
+#define SD_EIG2_MIN_BLOCKS 1  // __launch_bounds__ minimum resident blocks (register cap)
+#endif
 constexpr int kEig2Rows = SD_EIG2_ROWS;
 constexpr int kEig2Threads = SD_EIG2_THREADS;
 constexpr int kEig2Stages = SD_EIG2_STAGES;
@@ -831,7 +834,7 @@ __device__ __forceinline__ void eig2_load(const double* __restrict__ A, int64_t 
 }
 
 template <bool kVec, bool kReport>
-__global__ void __launch_bounds__(kEig2Threads) eig2_kernel(const double* __restrict__ A, int64_t n,
+__global__ void __launch_bounds__(kEig2Threads, SD_EIG2_MIN_BLOCKS) eig2_kernel(const double* __restrict__ A, int64_t n,
                                                             double* __restrict__ lam,
                                                             double* __restrict__ phi,
                                                             uint8_t* __restrict__ status,

@@ -28,19 +28,17 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants2"
 VARIANTS = {
     "literal_r1_t128": {"SD_EIG2_LITERAL": 1, "SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1,
                         "SD_EIG2_THREADS": 128},
-    "tile_r1_t128": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 128},
     "tile_r2_t128": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128},
-    "tile_r4_t128": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 4, "SD_EIG2_THREADS": 128},
-    "stream_r1_t256_b4": {"SD_EIG2_MODE": 1, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 256,
-                          "SD_EIG2_BLOCKS_PER_SM": 4},
-    "stream_r2_t256_b2": {"SD_EIG2_MODE": 1, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 256,
-                          "SD_EIG2_BLOCKS_PER_SM": 2},
-    "stream_r2_t128_b5": {"SD_EIG2_MODE": 1, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
-                          "SD_EIG2_BLOCKS_PER_SM": 5},
-    "stream_r2_t256_b3_nopf": {"SD_EIG2_MODE": 1, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 256,
-                               "SD_EIG2_BLOCKS_PER_SM": 3, "SD_EIG2_PREFETCH": 0},
-    "bulk_t256_s3_b4": {"SD_EIG2_MODE": 2, "SD_EIG2_THREADS": 256, "SD_EIG2_STAGES": 3,
-                        "SD_EIG2_BLOCKS_PER_SM": 4},
+    "tile_r2_t128_mb12": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
+                          "SD_EIG2_MIN_BLOCKS": 12},
+    "tile_r2_t128_mb16": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
+                          "SD_EIG2_MIN_BLOCKS": 16},
+    "tile_r1_t128_mb12": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 128,
+                          "SD_EIG2_MIN_BLOCKS": 12},
+    "tile_r1_t128_mb16": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 128,
+                          "SD_EIG2_MIN_BLOCKS": 16},
+    "tile_r3_t128_mb10": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 3, "SD_EIG2_THREADS": 128,
+                          "SD_EIG2_MIN_BLOCKS": 10},
 }
 
 
