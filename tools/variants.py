@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "gate_libm": {"SD_FAST_GATE_POLY": 0},
+    "win_cos": {"SD_FAST_WIN_SQRT": 0},
 }
 
 
