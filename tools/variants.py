@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "win_cos": {"SD_FAST_WIN_SQRT": 0},
+    "win_alg": {"SD_FAST_WIN_ALG": 1},
 }
 
 
