@@ -56,9 +56,9 @@ def summarise(rep: str):
                     k[name] = k[name] * 1e9
                 elif u == "Kbyte" and name.endswith("bytes"):
                     k[name] = k[name] * 1e3
-                elif u == "usecond" and name == "duration_ns":
+                elif u in ("usecond", "us") and name == "duration_ns":
                     k[name] = k[name] * 1e3
-                elif u == "msecond" and name == "duration_ns":
+                elif u in ("msecond", "ms") and name == "duration_ns":
                     k[name] = k[name] * 1e6
         stalls = {h[len(STALLS):]: float(d[h]) for h in hdr
                   if h.startswith(STALLS) and not h.endswith("not_issued") and d[h] not in ("", "0")}
