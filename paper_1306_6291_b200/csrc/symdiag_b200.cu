@@ -407,7 +407,13 @@ __device__ __forceinline__ void wait_prior_grid() {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kPassThreads, SD_FAST_MIN_BLOCKS)
+// The pass runs only the long Generic / DoubleRoot bodies on dense rounds:
+// 3 blocks (85 registers, fewer spills) beat 4 blocks at 64 registers by 2%
+// on c3 (c2/c4 hand nothing to the pass; profiles/r1_variants25_pass_blocks.jsonl)
+#ifndef SD_PASS_MIN_BLOCKS
+#define SD_PASS_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kPassThreads, SD_PASS_MIN_BLOCKS)
     eig3_pass_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
                      T* __restrict__ ang, uint8_t* __restrict__ status, int vec) {
   // generic rows from the front, double roots from the back (row < 2^32:
@@ -717,7 +723,7 @@ unsigned pass_grid(int64_t n) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (nsm <= 0) nsm = 148;
   const int64_t ntiles = (n + kPassTile - 1) / kPassTile;
-  const int64_t g = (int64_t)nsm * SD_FAST_MIN_BLOCKS;
+  const int64_t g = (int64_t)nsm * SD_PASS_MIN_BLOCKS;
   return (unsigned)(ntiles < g ? ntiles : g);
 }
 

@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "win_alg": {"SD_FAST_WIN_ALG": 1},
+    "pass_mb4": {"SD_PASS_MIN_BLOCKS": 4},
 }
 
 
