@@ -25,7 +25,8 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "pass_mb4": {"SD_PASS_MIN_BLOCKS": 4},
+    "dbl64": {"SD_PASS_MIN_DBL": 64},
+    "dbl192": {"SD_PASS_MIN_DBL": 192},
 }
 
 
