@@ -25,8 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "dbl64": {"SD_PASS_MIN_DBL": 64},
-    "dbl192": {"SD_PASS_MIN_DBL": 192},
+    "polish_libm": {"SD_POLISH_POLY": 0},
 }
 
 
