@@ -549,7 +549,7 @@ def main():
     if not args.no_e2e:
         # e2e through the public host-buffer C-ABI path (every rank)
         barrier()
-        times, h2d, d2h = run_e2e(sd, cfg, n, max(2, args.steps // 5), 1, dev.index)
+        times, h2d, d2h = run_e2e(sd, cfg, n, max(5, args.steps // 2), 2, dev.index)
         tmax = statistics.median(times)
         if dist is not None:
             t = torch.tensor([tmax], dtype=torch.float64)
