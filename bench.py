@@ -230,6 +230,13 @@ def run_hot(sd, A, steps, warmup, config):
         s.record(stream)
         fn()
         e.record(stream)
+        if flush is not None:
+            # microsecond-scale calls: wait here (outside the events) so the
+            # next iteration's flush is on the GPU while the host enqueues the
+            # timed call; otherwise the host's enqueue lag for the Python call
+            # can land between the start event and the kernel
+            # (tools/c1_timing_probe.py: 15.0 vs 14.1 us per c1 call)
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     launches = sd._lib.launch_count() - l0
     per = [s.elapsed_time(e) for s, e in ev]
