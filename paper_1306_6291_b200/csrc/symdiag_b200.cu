@@ -239,14 +239,18 @@ __device__ __forceinline__ void unstash_lam(const T* lam, const T* ang, int64_t 
 template <typename T>
 __device__ __forceinline__ void store_fast(T* lam, T* ang, uint8_t* status, int64_t r, int rc,
                                           const double l[3], const double phi[3], uint8_t st) {
-  if (rc == sd::kFastDone || rc == sd::kFastPolish) {
-    // done, or closed form written with the polish pending (fp32: the
-    // polish pass recomputes the fp64 closed form itself)
+  if (rc == sd::kFastDone || (rc == sd::kFastPolish && sizeof(T) == 8)) {
+    // done, or the fp64 closed form written with the polish pending
 #pragma unroll
     for (int k = 0; k < 3; k++) {
       lam[3 * r + k] = (T)l[k];
       ang[3 * r + k] = (T)phi[k];
     }
+  } else if (rc == sd::kFastPolish) {
+    // fp32 outputs cannot carry the fp64 closed form: the fp64 angles wait
+    // in the row's 24 output bytes, the polish pass recomputes lambda
+    // (classify3, deterministic) instead of the whole closed form
+    stash_lam<T>(lam, ang, r, phi);
   } else if (rc == sd::kFastError) {
 #pragma unroll
     for (int k = 0; k < 3; k++) lam[3 * r + k] = ang[3 * r + k] = (T)sd::qnan();
@@ -558,22 +562,23 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
         ph[q] = (double)ang[3 * i + q];
       }
     } else {
-      // fp32 outputs cannot carry the fp64 closed form from the fast kernel:
-      // recompute it here (same code, same inputs, same result)
+      // fp32: the fast kernel stashed the fp64 angles in the row's output
+      // bytes (store_fast); lambda comes from classify3 again (same code,
+      // same inputs, same value).  TripleRoot rows have zero angles.
       double scale = 1.0;
-      int reason = 0, rc = sd::kFastDefer;
+      int reason = 0;
       const int cls = sd::classify3(a, lm, scale, reason);
-      if (cls == 4) {
-        ph[0] = ph[1] = ph[2] = 0.0;
-        rc = sd::kFastPolish;
-      } else if (cls == 0) {
-        rc = sd::fast_generic(a, scale, lm, ph, st);
-      } else if (cls == 3) {
-        rc = sd::fast_double(a, scale, lm, ph, st);
-      }
-      if (rc != sd::kFastPolish) {  // cannot happen; the literal pass is the safety net
+      const int pc = st & SD_CODE_MASK;
+      const bool ok = pc == sd::kPolishTriple ? cls == 4
+                                               : (pc == sd::kPolishDouble ? cls == 3 : cls == 0);
+      if (!ok) {  // cannot happen; the literal pass is the safety net
         status[i] = (uint8_t)(sd::kDeferred | (11 << 4));
         return;
+      }
+      if (pc == sd::kPolishTriple) {
+        ph[0] = ph[1] = ph[2] = 0.0;
+      } else {
+        unstash_lam<T>(lam, ang, i, ph);
       }
 #pragma unroll
       for (int q = 0; q < 3; q++) {
