@@ -626,8 +626,15 @@ __device__ __forceinline__ unsigned fix_mine4(unsigned w) {
          ~__vcmpeq4(w, 0x01010101u * sd::kDblPending);
 }
 
+// The literal pass (kPolish = false) runs the whole reference solver for a
+// few rows: SD_LIT_MIN_BLOCKS resident blocks (register cap vs spills; 2, 3,
+// 6, 8 measured no better than 4, profiles/r1_variants28_literal_blocks.jsonl).
+#ifndef SD_LIT_MIN_BLOCKS
+#define SD_LIT_MIN_BLOCKS SD_FIX_MIN_BLOCKS
+#endif
 template <typename T, bool kPolish>
-__global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_kernel(const T* __restrict__ A,
+__global__ void __launch_bounds__(kFixThreads, kPolish ? SD_FIX_MIN_BLOCKS : SD_LIT_MIN_BLOCKS)
+    eig3_fixup_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
                                                                  uint8_t* __restrict__ status,
@@ -691,13 +698,13 @@ __global__ void __launch_bounds__(kFixThreads, SD_FIX_MIN_BLOCKS) eig3_fixup_ker
   for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kPolish>(A, lam, ang, status, queue[k]);
 }
 
-int fixup_grid(int64_t n) {
+int fixup_grid(int64_t n, int blocks_per_sm) {
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (nsm <= 0) nsm = 148;
   const int64_t ntiles = (n + kFixTile - 1) / kFixTile;
-  const int64_t g = (int64_t)nsm * SD_FIX_MIN_BLOCKS;
+  const int64_t g = (int64_t)nsm * blocks_per_sm;
   return (int)(ntiles < g ? ntiles : g);
 }
 
@@ -1297,7 +1304,8 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
     eig3_fast_kernel<T, false><<<g1, kFastThreads, 0, s>>>(A, n, lam, ang, status);
   int rc = check_launch("eig3_fast_kernel");
   if (rc != SD_OK) return rc;
-  const unsigned g2 = (unsigned)fixup_grid(n);
+  const unsigned g2 = (unsigned)fixup_grid(n, SD_FIX_MIN_BLOCKS);
+  const unsigned g3 = (unsigned)fixup_grid(n, SD_LIT_MIN_BLOCKS);
   const int vec = aligned(status, 16) ? 1 : 0;
   if (SD_PASS) {
     launch_after(eig3_pass_kernel<T>, pass_grid(n), kPassThreads, s, A, n, lam, ang, status,
@@ -1308,7 +1316,7 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   launch_after(eig3_fixup_kernel<T, true>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;
-  launch_after(eig3_fixup_kernel<T, false>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
+  launch_after(eig3_fixup_kernel<T, false>, g3, kFixThreads, s, A, n, lam, ang, status, vec);
   return check_launch("eig3_literal_kernel");
 }
 

@@ -25,7 +25,8 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "polish_libm": {"SD_POLISH_POLY": 0},
+    "lit6": {"SD_LIT_MIN_BLOCKS": 6},
+    "lit8": {"SD_LIT_MIN_BLOCKS": 8},
 }
 
 
