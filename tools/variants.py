@@ -25,8 +25,8 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "lit6": {"SD_LIT_MIN_BLOCKS": 6},
-    "lit8": {"SD_LIT_MIN_BLOCKS": 8},
+    "rows2": {"SD_FAST_ROWS": 2},
+    "rows3": {"SD_FAST_ROWS": 3},
 }
 
 
