@@ -25,8 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "rows2": {"SD_FAST_ROWS": 2},
-    "rows3": {"SD_FAST_ROWS": 3},
+    "win_merge": {"SD_FAST_WIN_MERGE": 1},
 }
 
 
