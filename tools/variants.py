@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "win_merge": {"SD_FAST_WIN_MERGE": 1},
+    "no_pass": {"SD_PASS": 0},
 }
 
 
