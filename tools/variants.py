@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "no_pass": {"SD_PASS": 0},
+    "py_hypot": {"SD_FAST_HYPOT": 0},
 }
 
 
