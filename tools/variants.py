@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "py_hypot": {"SD_FAST_HYPOT": 0},
+    "libdiv": {"SD_FAST_FDIV": 0},
 }
 
 
