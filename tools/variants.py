@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "libm_sqrt": {"SD_FAST_FSQRT": 0},
+    "libm_sincos": {"SD_FAST_SINCOS": 0},
 }
 
 
