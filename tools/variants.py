@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "libm_sincos": {"SD_FAST_SINCOS": 0},
+    "libm_eig_cos": {"SD_FAST_EIG_COSR": 0},
 }
 
 
