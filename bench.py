@@ -243,6 +243,13 @@ def run_hot(sd, A, steps, warmup, config):
     return per, launches, out
 
 
+def iq_mean(xs):
+    """Mean of the middle half of the samples."""
+    xs = sorted(xs)
+    k = len(xs) // 4
+    return statistics.mean(xs[k:len(xs) - k])
+
+
 def copy_floor(A, steps):
     """Mean event-timed ms of a device copy of A (same flush as run_hot)."""
     import torch
@@ -263,7 +270,7 @@ def copy_floor(A, steps):
         e.record(stream)
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
-    return statistics.mean(ts)
+    return iq_mean(ts)
 
 
 def run_sweep(sd, dev, steps=3):
@@ -579,9 +586,10 @@ def main():
             Ac = make_inputs(c, nc, dev, 0)
             small = COST[c]["bytes"] * nc < 4 * L2_BYTES
             pc, _, oc = run_hot(sd, Ac, 30 if small else 5, 3, c)
-            # event timestamps are quantised (~1 us) on this part: the mean
-            # of 30 calls for the microsecond-scale c1 call
-            kt = (statistics.mean(pc) if small else statistics.median(pc)) * 1e-3
+            # event timestamps are quantised (~1 us) on this part: for the
+            # microsecond-scale c1 call the interquartile mean of 30 calls
+            # (fine-grained like a mean, robust to a stray slow call like a median)
+            kt = (iq_mean(pc) if small else statistics.median(pc)) * 1e-3
             cc = COST[c]
             ach = 2.0 * cc["W"] * nc / kt / 1e12
             extra[c] = {"workload": workloads.CONFIGS[c]["desc"], "n": nc,
@@ -597,7 +605,8 @@ def main():
                 fl = copy_floor(Ac, 30)
                 extra[c]["copy_floor"] = {
                     "ms": fl, "what": "torch copy_ of the input (same bytes read + written), "
-                                      "same flush, mean of 30 event-timed calls",
+                                      "same flush, interquartile mean of 30 event-timed "
+                                      "calls",
                     "kernel_over_copy": kt * 1e3 / fl}
             del Ac, oc
             torch.cuda.empty_cache()
