@@ -90,6 +90,26 @@ __device__ __forceinline__ double div_nz(double a, double b) {
   return a / b;
 }
 
+// x**3 and x**6 exactly as pow3 / pow6 for |x| below 2^160 (the fast
+// path's guard), where neither can overflow: the same arithmetic without the
+// overflow tests
+__device__ __forceinline__ double pow3_nc(double x) {
+  const double h = __dmul_rn(x, x);
+  const double l = fma(x, x, -h);
+  const double hi = __dmul_rn(h, x);
+  const double lo = fma(h, x, -hi) + __dmul_rn(l, x);
+  return hi + lo;
+}
+__device__ __forceinline__ double pow6_nc(double x) {
+  const double h = __dmul_rn(x, x);
+  const double l = fma(x, x, -h);
+  const double c = __dmul_rn(h, x);
+  const double s = __dmul_rn(c, c);
+  const double cl = fma(h, x, -c) + __dmul_rn(l, x);
+  const double sl = fma(c, c, -s) + 2.0 * __dmul_rn(c, cl);
+  return s + sl;
+}
+
 // math_1 rules: NaN from non-NaN -> ValueError (math domain error)
 __device__ __forceinline__ double chk(Err& e, double r, double x) {
   if (is_nan(r) && !is_nan(x)) e.raise(SD_ERR_MATH_DOMAIN);

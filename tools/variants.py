@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "fast": {},
-    "libm_eig_cos": {"SD_FAST_EIG_COSR": 0},
+    "pow_checked": {"SD_FAST_POW_NC": 0},
 }
 
 
