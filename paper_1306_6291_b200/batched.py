@@ -55,18 +55,20 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else t.data_ptr()
 
 
-def _stream(stream=None, inputs=()) -> int:
+def _stream(stream=None, tensors=()) -> int:
     """Raw handle of the launch stream.  With an explicit `stream` other than
     the current one, the launch first waits for the current stream (where
-    the inputs, and any contiguous copies of them, were produced) and the
-    inputs are recorded on `stream` so the caching allocator cannot recycle
-    them before the kernel has read them."""
+    the inputs, any contiguous copies of them and the freshly allocated
+    outputs were produced) and every tensor the kernel reads or writes is
+    recorded on `stream`, so the caching allocator cannot hand its memory to
+    current-stream work before the kernel is done with it."""
     cur = torch.cuda.current_stream()
     if stream is None or stream == cur:
         return cur.cuda_stream
     stream.wait_stream(cur)
-    for t in inputs:
-        t.record_stream(stream)
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
     return stream.cuda_stream
 
 
@@ -122,13 +124,14 @@ def diagonalize3_batched(A: torch.Tensor, *, report: bool = False, with_d: bool 
             rep = _alloc(out, "report", (n, REPORT_STRIDE), torch.float64, dev) if report else None
             d = _alloc(out, "d", (n, 9), torch.float64, dev) if with_d else None
             _lib.call("sd_eig3_report_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
-                      st.data_ptr(), _ptr(rep), _ptr(d), _stream(stream, (A,)))
+                      st.data_ptr(), _ptr(rep), _ptr(d),
+                      _stream(stream, (A, lam, ang, st, rep, d)))
         elif dt == torch.float64:
             _lib.call("sd_eig3_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
-                      st.data_ptr(), _stream(stream, (A,)))
+                      st.data_ptr(), _stream(stream, (A, lam, ang, st)))
         else:
             _lib.call("sd_eig3_f32", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(),
-                      st.data_ptr(), _stream(stream, (A,)))
+                      st.data_ptr(), _stream(stream, (A, lam, ang, st)))
     return Eig3Batch(lam, ang, st, rep, d)
 
 
@@ -145,11 +148,58 @@ def diagonalize2_batched(A: torch.Tensor, *, with_d: bool = False,
         if with_d:
             d = _alloc(out, "d", (n, 4), torch.float64, dev)
             _lib.call("sd_eig2_report_f64", A.data_ptr(), n, lam.data_ptr(), phi.data_ptr(),
-                      st.data_ptr(), d.data_ptr(), _stream(stream, (A,)))
+                      st.data_ptr(), d.data_ptr(), _stream(stream, (A, lam, phi, st, d)))
         else:
             _lib.call("sd_eig2_f64", A.data_ptr(), n, lam.data_ptr(), phi.data_ptr(),
-                      st.data_ptr(), _stream(stream, (A,)))
+                      st.data_ptr(), _stream(stream, (A, lam, phi, st)))
     return Eig2Batch(lam, phi, st, d)
+
+
+def shard_to_devices(A, devices, pin: bool = True) -> list:
+    """Contiguous shards of host rows A[n, w] (numpy or CPU tensor), one per
+    entry of `devices` (shard_range: sizes differ by at most one row), each
+    copied to its device (from pinned memory, asynchronously on that
+    device's current stream).  Returns the list of device tensors."""
+    from .shard import shard_range
+    _lib.require_cuda()
+    if not isinstance(A, torch.Tensor):
+        A = torch.from_numpy(A)
+    if A.is_cuda:
+        raise ValueError("shard_to_devices takes host rows")
+    n, world = A.shape[0], len(devices)
+    ndev = torch.cuda.device_count()
+    for d in devices:
+        if not 0 <= int(d) < ndev:
+            raise _lib.CudaUnavailable(f"device {d} requested, {ndev} visible")
+    out = []
+    for r, d in enumerate(devices):
+        a, b = shard_range(n, r, world)
+        part = A[a:b]
+        if pin:
+            part = part.pin_memory()
+        with torch.cuda.device(int(d)):
+            out.append(part.to(torch.device("cuda", int(d)), non_blocking=pin))
+    return out
+
+
+def diagonalize3_batched_multi(shards: list, *, outs: Optional[list] = None,
+                               streams: Optional[list] = None) -> list:
+    """One process, several GPUs: `shards[i]` is a packed [n_i, 6]
+    CUDA tensor on its own device (e.g. from `shard_to_devices`).  Every
+    shard is launched asynchronously on its device's current stream (or
+    `streams[i]`), with no collective and no synchronisation: each GPU's
+    outputs stay on that GPU.  Returns one Eig3Batch per shard; row order
+    within a shard is the input order, so the concatenation over shards is
+    the single-call result for the concatenated input bit for bit."""
+    res = []
+    for i, A in enumerate(shards):
+        if not isinstance(A, torch.Tensor) or not A.is_cuda:
+            raise TypeError("diagonalize3_batched_multi takes CUDA tensors")
+        with torch.cuda.device(A.device):
+            res.append(diagonalize3_batched(
+                A, out=None if outs is None else outs[i],
+                stream=None if streams is None else streams[i]))
+    return res
 
 
 def _empty(n, w, dev, dtype=torch.float64):

@@ -75,6 +75,14 @@ int run_pipeline(sd_plan* plan, const Tin* A, int64_t n, int win, Tout* out0, in
     return herr(SD_EINVAL, "sd_*_host: bad argument", cudaSuccess);
   if (n == 0) return SD_OK;
   DeviceGuard g(plan->device);
+  // on any error, wait for every stream before returning: copies already
+  // queued into the caller's (possibly pinned) host buffers must not still
+  // be running when the caller sees the error and frees or reuses them; the
+  // first error code (and sd_last_error) is kept
+  auto drain = [&](int rc) {
+    for (int b = 0; b < kBuf; b++) cudaStreamSynchronize(plan->stream[b]);
+    return rc;
+  };
   const int64_t chunk = plan->chunk;
   const int64_t nchunks = (n + chunk - 1) / chunk;
   for (int64_t c = 0; c < nchunks; c++) {
@@ -87,9 +95,9 @@ int run_pipeline(sd_plan* plan, const Tin* A, int64_t n, int win, Tout* out0, in
     Tout* d1 = static_cast<Tout*>(plan->ang[b]);
     cudaError_t e = cudaMemcpyAsync(din, A + r0 * win, (size_t)m * win * sizeof(Tin),
                                     cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return herr(SD_ECUDA, "H2D copy", e);
+    if (e != cudaSuccess) return drain(herr(SD_ECUDA, "H2D copy", e));
     int rc = launch(din, m, d0, d1, plan->st[b], s);
-    if (rc != SD_OK) return rc;  // sd_last_error() already set by the launcher
+    if (rc != SD_OK) return drain(rc);  // sd_last_error() already set by the launcher
     e = cudaMemcpyAsync(out0 + r0 * w0, d0, (size_t)m * w0 * sizeof(Tout),
                         cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess)
@@ -97,13 +105,14 @@ int run_pipeline(sd_plan* plan, const Tin* A, int64_t n, int win, Tout* out0, in
                           cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(status + r0, plan->st[b], (size_t)m, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return herr(SD_ECUDA, "D2H copy", e);
+    if (e != cudaSuccess) return drain(herr(SD_ECUDA, "D2H copy", e));
   }
+  int rc = SD_OK;
   for (int b = 0; b < kBuf; b++) {
     cudaError_t e = cudaStreamSynchronize(plan->stream[b]);
-    if (e != cudaSuccess) return herr(SD_ECUDA, "stream sync", e);
+    if (e != cudaSuccess && rc == SD_OK) rc = herr(SD_ECUDA, "stream sync", e);
   }
-  return SD_OK;
+  return rc;
 }
 
 }  // namespace

@@ -123,14 +123,30 @@ def generate(config: str, n: int | None = None, start: int = 0) -> np.ndarray:
         n = spec["n"] - start
     width = 3 if spec["dim"] == 2 else 6
     out = np.empty((n, width), dtype=spec["dtype"])
+    pieces = []
     pos = 0
     while pos < n:
-        row = start + pos
-        k, off = divmod(row, CHUNK)
+        k, off = divmod(start + pos, CHUNK)
         take = min(CHUNK - off, n - pos)
-        block = _CHUNKERS[config](spec["seed"], k, CHUNK)
-        out[pos:pos + take] = block[off:off + take]
+        pieces.append((pos, k, off, take))
         pos += take
+
+    def fill(piece):
+        p, k, off, take = piece
+        block = _CHUNKERS[config](spec["seed"], k, CHUNK)
+        out[p:p + take] = block[off:off + take]
+
+    if len(pieces) <= 2:
+        for piece in pieces:
+            fill(piece)
+        return out
+    # chunks are independent (own generator each): fill them on host
+    # threads (numpy's generators and ufuncs release the GIL); the values do
+    # not depend on the thread count
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(fill, pieces))
     return out
 
 

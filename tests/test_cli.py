@@ -225,3 +225,45 @@ def test_native_verify_matches_python_verify():
     for fn in (cli.cmd_verify, cli.cmd_verify_native):
         with pytest.raises(cli.ParseError):
             fn(io.StringIO(bad), io.StringIO(), 1e-9)
+
+
+def test_whole_line_chunks_cut_only_at_newlines():
+    """The chunk reader never splits a line, also with a tiny chunk size,
+    and applies universal newlines to raw bytes."""
+    text = "".join(f'{{"id": {k}, "a11": 1, "a22": 2, "a12": 0.{k}}}\n' for k in range(50))
+    got = list(cli._whole_line_chunks(io.StringIO(text + "tail"), chunk=7))
+    assert "".join(got) == text + "tail"
+    assert all(c.endswith("\n") for c in got[:-1]) and got[-1].endswith("tail")
+    raw = io.TextIOWrapper(io.BytesIO(text.replace("\n", "\r\n").encode()))
+    assert "".join(cli._whole_line_chunks(raw, chunk=11)) == text
+
+
+@gpu
+@pytest.mark.parametrize("codec", [[], ["--python-codec"]])
+def test_solve_streams_one_answer_per_line_over_a_pipe(codec):
+    """A pipe client sends one record and waits: the answer must arrive while
+    stdin is still open (the reference writes each result as its line
+    arrives, cli.py:117-137)."""
+    import os
+    import select
+    import subprocess
+    import sys
+    root = Path(__file__).resolve().parents[1]
+    p = subprocess.Popen([sys.executable, "-m", "paper_1306_6291_b200.cli", "solve", *codec],
+                         cwd=root, stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                         stderr=subprocess.PIPE)
+    try:
+        for k in range(2):
+            p.stdin.write(b'{"id": %d, "a11": 1, "a22": 2, "a33": 3, "a12": 0.5, '
+                          b'"a13": 0.25, "a23": 0.125}\n' % k)
+            p.stdin.flush()
+            ready, _, _ = select.select([p.stdout], [], [], 180)
+            assert ready, "no answer while stdin is open"
+            rec = json.loads(p.stdout.readline())
+            assert rec["id"] == k and rec["dim"] == 3
+        p.stdin.close()
+        assert p.wait(timeout=60) == 0
+        assert p.stdout.read() == b""
+    finally:
+        if p.poll() is None:
+            os.kill(p.pid, 9)

@@ -563,6 +563,25 @@ def test_single_process_multi_device_host_path():
     assert np.array_equal(st, ref.status.cpu().numpy())
 
 
+def test_device_resident_multi_shards_equal_single_call():
+    """diagonalize3_batched_multi over shard_to_devices (contiguous shards,
+    two on the same GPU here; one per GPU on a node): the concatenated
+    outputs equal one call over the whole batch bit for bit."""
+    A = workloads.generate("c3", 200_003)
+    ref = sd.diagonalize3_batched(torch.as_tensor(A).to(DEV))
+    shards = sd.shard_to_devices(A, [0, 0])
+    assert [s.shape[0] for s in shards] == [100_002, 100_001]
+    res = sd.diagonalize3_batched_multi(shards)
+    torch.cuda.synchronize()
+    for k in ("lam", "ang", "status"):
+        got = torch.cat([getattr(r, k) for r in res])
+        assert torch.equal(torch.nan_to_num(got, nan=7.0) if got.is_floating_point() else got,
+                           torch.nan_to_num(getattr(ref, k), nan=7.0)
+                           if got.is_floating_point() else getattr(ref, k)), k
+    with pytest.raises(sd.CudaUnavailable):
+        sd.shard_to_devices(A, [0, torch.cuda.device_count()])
+
+
 @pytest.mark.parametrize("n", [1, 31, 257, 4099])
 def test_no_writes_outside_outputs(n):
     """Out-of-bounds write check (compute-sanitizer is not available on the

@@ -69,7 +69,36 @@ def summarise(rep: str):
     return out
 
 
+def update_profile_summary(rep: str, config: str, n: int, path: str, source: str,
+                           bytes_per_row: int):
+    """Write profiles/ncu_summary.json[config] from the kernels of ONE call
+    (the captured launches of one sd_eig3 / sd_eig2 call, in launch order):
+    per-kernel metrics, DRAM bytes per call and the executed FP64
+    thread-instructions per row that bench.py's roofline uses."""
+    import os
+    ks = summarise(rep)
+    doc = json.load(open(path)) if os.path.exists(path) else {}
+    dram = sum(k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0) for k in ks)
+    fp64 = sum(k.get("dfma_thread_inst", 0) + k.get("dmul_thread_inst", 0)
+               + k.get("dadd_thread_inst", 0) for k in ks)
+    doc[config] = {"n": n, "dram_bytes_per_launch": dram,
+                   "algorithmic_bytes_per_launch": bytes_per_row * n,
+                   "fp64_thread_inst_per_row": fp64 / n, "kernels": ks, "source": source}
+    json.dump(doc, open(path, "w"), indent=1)
+    return doc[config]
+
+
 if __name__ == "__main__":
+    if "--config" in sys.argv:
+        a = sys.argv
+        cfg = a[a.index("--config") + 1]
+        n = int(a[a.index("--n") + 1])
+        out = a[a.index("--out") + 1] if "--out" in a else "profiles/ncu_summary.json"
+        src = a[a.index("--source") + 1] if "--source" in a else a[1]
+        bpr = int(a[a.index("--bytes-per-row") + 1]) if "--bytes-per-row" in a else 96
+        r = update_profile_summary(a[1], cfg, n, out, src, bpr)
+        print(json.dumps({k: v for k, v in r.items() if k != "kernels"}))
+        sys.exit(0)
     res = summarise(sys.argv[1])
     if "--json" in sys.argv:
         json.dump(res, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
