@@ -254,13 +254,13 @@ def test_solve_streams_one_answer_per_line_over_a_pipe(codec):
                          stderr=subprocess.PIPE)
     try:
         for k in range(2):
-            p.stdin.write(b'{"id": %d, "a11": 1, "a22": 2, "a33": 3, "a12": 0.5, '
+            p.stdin.write(b'{"id": "r%d", "a11": 1, "a22": 2, "a33": 3, "a12": 0.5, '
                           b'"a13": 0.25, "a23": 0.125}\n' % k)
             p.stdin.flush()
             ready, _, _ = select.select([p.stdout], [], [], 180)
             assert ready, "no answer while stdin is open"
             rec = json.loads(p.stdout.readline())
-            assert rec["id"] == k and rec["dim"] == 3
+            assert rec["id"] == f"r{k}" and rec["dim"] == 3, rec
         p.stdin.close()
         assert p.wait(timeout=60) == 0
         assert p.stdout.read() == b""
