@@ -174,6 +174,14 @@ int sd_residuals_f64(int dim, const double* A, const double* lam, const double* 
 int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots,
                        uint8_t* status, void* cuda_stream);
 
+/* x[i] ** y[i] with the reference's pow: CPython float ** float is libm
+ * pow, i.e. glibc 2.39's pow (e_pow.c, the FMA build on x86-64), restated
+ * bit for bit for the device (csrc/sd_glibc_pow.h); y integer-valued with
+ * 2^-65 <= |y| < 2^63 (the reference raises to 2, 3 and 6).  Replaces the
+ * `**` of eig3.py:89, 99, 105-108, 140, 147, 151 and core.py:107-108.     */
+int sd_glibc_pow_f64(const double* x, const double* y, int64_t n, double* out,
+                     void* cuda_stream);
+
 /* ---- host-buffer path (end-to-end: H2D, kernel, D2H, pipelined) ---------- */
 typedef struct sd_plan sd_plan;
 /* A plan owns three device staging slots of `chunk` matrices and three CUDA

@@ -38,6 +38,7 @@ SIGNATURES = {
     "sd_jacobi_f64": [_I, _P, _I64, ctypes.c_double, _P, _P, _P, _P, _P, _P],
     "sd_residuals_f64": [_I, _P, _P, _P, _I64, _P, _P],
     "sd_cubic_roots_f64": [_P, _I64, _P, _P, _P],
+    "sd_glibc_pow_f64": [_P, _P, _I64, _P, _P],
     "sd_plan_create": [_I, _I64, ctypes.POINTER(_P)],
     "sd_eig3_report_f64_host": [_P, _P, _I64, _P, _P, _P, _P, _P],
     "sd_eig2_report_f64_host": [_P, _P, _I64, _P, _P, _P, _P],

@@ -370,6 +370,23 @@ def cubic_roots_batched(bcd: torch.Tensor):
     return roots, st
 
 
+def glibc_pow_batched(x: torch.Tensor, y) -> torch.Tensor:
+    """x ** y elementwise with the reference's pow (glibc 2.39 restated,
+    csrc/sd_glibc_pow.h): bit-identical to CPython's float ** on the
+    reference's host; y a scalar or tensor of integer-valued exponents."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64:
+        raise TypeError("x must be a CUDA float64 tensor")
+    x = x.contiguous().view(-1)
+    y = (torch.full_like(x, float(y)) if not isinstance(y, torch.Tensor)
+         else y.to(device=x.device, dtype=torch.float64).contiguous().view(-1))
+    _same_rows(x.shape[0], x.device, y)
+    out = torch.empty_like(x)
+    with torch.cuda.device(x.device):
+        _lib.call("sd_glibc_pow_f64", x.data_ptr(), y.data_ptr(), x.shape[0], out.data_ptr(),
+                  _stream())
+    return out
+
+
 class HostPlan:
     """End-to-end path over HOST buffers (numpy or pinned torch CPU tensors):
     chunked H2D -> kernel -> D2H, pipelined over three streams in C++

@@ -6,9 +6,9 @@
 // one contraction in p = b*b - 3c flips 20% of near-triple branches).
 //
 // What is reproduced exactly, and how:
-//   x**2          -> x*x (correctly rounded; glibc pow(x,2) differs in ~0.09%
-//                    of calls by one ulp — harmless)
-//   x**3, x**6    -> double-double products, one final rounding
+//   x**2, x**3, x**6 -> glibc 2.39's pow restated bit for bit
+//                    (sd_glibc_pow.h); the fast path evaluates correctly
+//                    rounded powers and bounds their one-ulp difference
 //   math.hypot    -> CPython 3.12 vector_norm algorithm (exact restatement)
 //   math.remainder-> CUDA remainder (exact, as glibc)
 //   math.sqrt     -> IEEE sqrt (correctly rounded, as glibc)
@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "../../include/symdiag_b200.h"
+#include "sd_glibc_pow.h"
 
 namespace sd {
 
@@ -43,44 +44,22 @@ __device__ __forceinline__ bool is_nan(double x) { return x != x; }
 __device__ __forceinline__ bool is_inf(double x) { return fabs(x) == __longlong_as_double(0x7ff0000000000000LL); }
 __device__ __forceinline__ bool is_finite(double x) { return fabs(x) < __longlong_as_double(0x7ff0000000000000LL); }
 
-// float ** 2 with CPython's OverflowError rule
-__device__ __forceinline__ double pow2(Err& e, double x) {
-  double r = __dmul_rn(x, x);
+// glibc 2.39's pow, bit for bit (sd_glibc_pow.h; tests/test_glibc_pow.py
+// checks the same source against the host libm), one out-of-line copy
+__device__ __noinline__ double glibc_pow(double x, double y) { return sd_glibc::pow(x, y); }
+
+// float ** k with CPython's OverflowError rule (float_pow: a finite base
+// whose libm pow overflows raises; an underflow does not).  Exact: the
+// reference's `x**k` is libm pow, whose last bit decides branches and
+// signs (sd_glibc_pow.h).
+__device__ __forceinline__ double pow_k(Err& e, double x, double k) {
+  const double r = glibc_pow(x, k);
   if (is_inf(r) && is_finite(x)) e.raise(SD_ERR_OVERFLOW);
   return r;
 }
-// x**3, correctly rounded up to a ~2^-104 relative window.  When the
-// leading product overflows, the error terms are inf - inf = NaN, so the
-// overflow is detected on the leading product (CPython: OverflowError).
-__device__ __forceinline__ double pow3(Err& e, double x) {
-  double h = __dmul_rn(x, x);
-  double l = fma(x, x, -h);
-  double hi = __dmul_rn(h, x);
-  if (!is_finite(hi)) {
-    if (is_finite(x)) e.raise(SD_ERR_OVERFLOW);
-    return hi;
-  }
-  double lo = fma(h, x, -hi) + __dmul_rn(l, x);
-  double r = hi + lo;
-  if (is_inf(r) && is_finite(x)) e.raise(SD_ERR_OVERFLOW);
-  return r;
-}
-// x**6 as (x^3)^2 in double-double
-__device__ __forceinline__ double pow6(Err& e, double x) {
-  double h = __dmul_rn(x, x);
-  double l = fma(x, x, -h);
-  double c = __dmul_rn(h, x);
-  double s = __dmul_rn(c, c);
-  if (!is_finite(s)) {
-    if (is_finite(x)) e.raise(SD_ERR_OVERFLOW);
-    return s;
-  }
-  double cl = fma(h, x, -c) + __dmul_rn(l, x);  // x^3 = c + cl
-  double sl = fma(c, c, -s) + 2.0 * __dmul_rn(c, cl);
-  double r = s + sl;
-  if (is_inf(r) && is_finite(x)) e.raise(SD_ERR_OVERFLOW);
-  return r;
-}
+__device__ __forceinline__ double pow2(Err& e, double x) { return pow_k(e, x, 2.0); }
+__device__ __forceinline__ double pow3(Err& e, double x) { return pow_k(e, x, 3.0); }
+__device__ __forceinline__ double pow6(Err& e, double x) { return pow_k(e, x, 6.0); }
 
 // a / b, with a == +-0 over a non-zero, non-NaN b answered without the
 // division (the same signed zero): libdevice's correctly rounded division
@@ -90,9 +69,10 @@ __device__ __forceinline__ double div_nz(double a, double b) {
   return a / b;
 }
 
-// x**3 and x**6 exactly as pow3 / pow6 for |x| below 2^160 (the fast
-// path's guard), where neither can overflow: the same arithmetic without the
-// overflow tests
+// Correctly rounded x**3 and x**6 (double-double products, one final
+// rounding; the fast path's first-level values, |x| below 2^160 so neither
+// can overflow).  glibc's pow can differ from them by one ulp: the fast
+// path bounds that difference in every decision (sd_fast3.cuh, classify3)
 __device__ __forceinline__ double pow3_nc(double x) {
   const double h = __dmul_rn(x, x);
   const double l = fma(x, x, -h);

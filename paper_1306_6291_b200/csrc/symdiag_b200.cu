@@ -1253,6 +1253,12 @@ __global__ void __launch_bounds__(256) residuals_kernel(const double* A, const d
   for (int k = 0; k < N + 2; k++) out[(N + 2) * i + k] = o[k];
 }
 
+// x ** y elementwise with the reference's pow (glibc 2.39, sd_glibc_pow.h)
+__global__ void glibc_pow_kernel(const double* x, const double* y, int64_t n, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = sd::glibc_pow(x[i], y[i]);
+}
+
 __global__ void cubic_roots_kernel(const double* bcd, int64_t n, double* roots,
                                    uint8_t* status) {
   const int64_t i = gtid();
@@ -1470,6 +1476,10 @@ int sd_residuals_f64(int dim, const double* A, const double* lam, const double* 
 int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots, uint8_t* status,
                        void* stream) {
   SIMPLE_LAUNCH(cubic_roots_kernel, bcd, n, roots, status);
+}
+
+int sd_glibc_pow_f64(const double* x, const double* y, int64_t n, double* out, void* stream) {
+  SIMPLE_LAUNCH(glibc_pow_kernel, x, y, n, out);
 }
 
 int sd_probe_dfma(int blocks, int iters, double* sink, double* dfma_total, void* stream) {

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import io
 import json
+import math
 import os
 
 import numpy as np
@@ -294,6 +295,32 @@ def test_stage_kernels_match_reference(name):
     st = st.cpu().numpy()
     vst = g["vw_status"][ok2]
     assert np.array_equal(st[st != 0], vst[st != 0])
+
+
+def test_device_glibc_pow_bit_exact():
+    """The device's pow (csrc/sd_glibc_pow.h, every `**` of the literal path)
+    against the host's libm pow — CPython's `x ** k` — bit for bit, for the
+    reference's exponents 2, 3, 6 over normal, tiny, huge, negative,
+    subnormal and overflowing bases."""
+    rng = np.random.default_rng(11)
+    parts = [rng.standard_normal(200_000),
+             rng.standard_normal(100_000) * 10.0 ** rng.integers(-160, 160, 100_000),
+             rng.uniform(-10, 10, 100_000),
+             np.ldexp(rng.uniform(1, 2, 20_000), rng.integers(-1074, -1000, 20_000)),
+             np.array([0.0, -0.0, 1.0, -1.0, 1e154, 1.4e154, 5.7e102, 1e-160, 1e-320,
+                       2.2250738585072014e-308, 3.0, -7.0])]
+    x = np.concatenate(parts)
+    for k in (2.0, 3.0, 6.0):
+        exp = []
+        for v in x.tolist():
+            try:
+                exp.append(v ** k)
+            except OverflowError:
+                exp.append(math.inf if (v > 0 or k % 2 == 0) else -math.inf)
+        exp = np.array(exp)
+        got = sd.glibc_pow_batched(torch.as_tensor(x).to(DEV), k).cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)), \
+            (k, int((got.view(np.uint64) != exp.view(np.uint64)).sum()))
 
 
 def test_error_rows_are_nan_and_coded():
