@@ -516,6 +516,108 @@ __device__ __forceinline__ double abs_residual(const double d[9], const double l
   return sqrt(s);
 }
 
+// numpy's j.T @ r for j[9][3] (OpenBLAS 0.3.30 dgemv_n, 3-row lda==3 tail:
+// column pairs in blocks of four, then the last column), bit for bit as
+// oracle/symdiag_oracle.c jt_resid (tools/polish_orders.py)
+__device__ __forceinline__ void jt_resid_ob(const double J[9][3], const double r[9], double out[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) t = t + fma(J[k][i], r[k], J[k + 1][i] * r[k + 1]);
+    out[i] = fma(J[8][i], r[8], t);
+  }
+}
+
+// np.linalg.solve for 3x3, one right-hand side: OpenBLAS's dgesv (getf2:
+// left-looking LU, reciprocal-scaled multipliers; getrs: laswp + column
+// axpys + divisions), bit for bit as oracle/symdiag_oracle.c solve3
+__device__ __forceinline__ void solve3_ob(const double m[9], const double rhs[3], double x[3]) {
+  double a[9];  // column-major
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) a[i + 3 * j] = m[3 * i + j];
+  int ipiv[3];
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    double* b = a + 3 * j;
+#pragma unroll
+    for (int i = 0; i < j; i++) {
+      const int jp = ipiv[i];
+      if (jp != i) {
+        const double t = b[i];
+        b[i] = b[jp];
+        b[jp] = t;
+      }
+    }
+#pragma unroll
+    for (int i = 1; i < j; i++) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; k++) t = fma(b[k], a[i + 3 * k], t);
+      b[i] = b[i] - t;
+    }
+#pragma unroll
+    for (int r = j; r < 3; r++) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < j; k++) t = fma(a[r + 3 * k], b[k], t);
+      b[r] = fma(-1.0, t, b[r]);
+    }
+    int jp = j;
+    double best = fabs(b[j]);
+#pragma unroll
+    for (int r = j + 1; r < 3; r++)
+      if (fabs(b[r]) > best) {
+        best = fabs(b[r]);
+        jp = r;
+      }
+    ipiv[j] = jp;
+    const double piv = b[jp];
+    if (piv != 0.0) {
+      if (jp != j)
+#pragma unroll
+        for (int k = 0; k <= j; k++) {
+          const double t = a[j + 3 * k];
+          a[j + 3 * k] = a[jp + 3 * k];
+          a[jp + 3 * k] = t;
+        }
+      if (fabs(piv) >= 0x1p-1022) {
+        const double rp = 1.0 / piv;
+#pragma unroll
+        for (int r = j + 1; r < 3; r++) b[r] = b[r] * rp;
+      } else {
+#pragma unroll
+        for (int r = j + 1; r < 3; r++) b[r] = b[r] / piv;
+      }
+    }
+  }
+  double y[3] = {rhs[0], rhs[1], rhs[2]};
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    const int jp = ipiv[i];
+    if (jp != i) {
+      const double t = y[i];
+      y[i] = y[jp];
+      y[jp] = t;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int k = i + 1; k < 3; k++) y[k] = fma(-y[i], a[k + 3 * i], y[k]);
+#pragma unroll
+  for (int i = 2; i >= 0; i--) {
+    y[i] = y[i] / a[i + 3 * i];
+#pragma unroll
+    for (int k = 0; k < i; k++) y[k] = fma(-y[i], a[k + 3 * i], y[k]);
+  }
+  x[0] = y[0];
+  x[1] = y[1];
+  x[2] = y[2];
+}
+
 // _polish_angles (eig3.py:463-489): two damped Gauss-Newton steps on the
 // angles, keeping the best.  Rare (0.02% of N(0,1), ~10% of the degenerate
 // config), so it is kept out of line to spare the hot path's registers.
@@ -575,49 +677,17 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
       mm3(rec, g, rg);
       for (int k = 0; k < 9; k++) J[k][c] = gr[k] - rg[k];
     }
-    double jtj[9], jtr[3];
-    for (int i = 0; i < 3; i++) {
+    double jtj[9], jtr[3], x[3];
+    for (int i = 0; i < 3; i++)
       for (int j = 0; j < 3; j++) {
         double s = J[0][i] * J[0][j];
         for (int k = 1; k < 9; k++) s = fma(J[k][i], J[k][j], s);
         jtj[3 * i + j] = s + (i == j ? damp : 0.0);
       }
-      double s = J[0][i] * (rec[0] - am[0]);
-      for (int k = 1; k < 9; k++) s = fma(J[k][i], rec[k] - am[k], s);
-      jtr[i] = s;
-    }
-    // LU with partial pivoting (LAPACK dgesv semantics)
-    for (int k = 0; k < 3; k++) {
-      int p = k;
-      double bestp = fabs(jtj[3 * k + k]);
-      for (int i = k + 1; i < 3; i++)
-        if (fabs(jtj[3 * i + k]) > bestp) {
-          bestp = fabs(jtj[3 * i + k]);
-          p = i;
-        }
-      if (p != k) {
-        for (int j = 0; j < 3; j++) {
-          double tt = jtj[3 * k + j];
-          jtj[3 * k + j] = jtj[3 * p + j];
-          jtj[3 * p + j] = tt;
-        }
-        double tt = jtr[k];
-        jtr[k] = jtr[p];
-        jtr[p] = tt;
-      }
-      double rp = 1.0 / jtj[3 * k + k];
-      for (int i = k + 1; i < 3; i++) {
-        double lf = jtj[3 * i + k] * rp;
-        for (int j = k + 1; j < 3; j++) jtj[3 * i + j] = jtj[3 * i + j] - lf * jtj[3 * k + j];
-        jtr[i] = jtr[i] - lf * jtr[k];
-      }
-    }
-    double x[3];
-    for (int i = 2; i >= 0; i--) {
-      double s = jtr[i];
-      for (int j = i + 1; j < 3; j++) s = s - jtj[3 * i + j] * x[j];
-      x[i] = s / jtj[3 * i + i];
-    }
+    double resid[9];
+    for (int k = 0; k < 9; k++) resid[k] = rec[k] - am[k];
+    jt_resid_ob(J, resid, jtr);
+    solve3_ob(jtj, jtr, x);
     for (int i = 0; i < 3; i++) cur[i] = cur[i] - x[i];
     compose_rotation(e, cur, d);
     recon(d, rec);

@@ -12,8 +12,8 @@ sys.path.insert(0, '.')
 import paper_1306_6291_b200 as sd
 from paper_1306_6291_b200 import workloads
 dev = torch.device('cuda', 0)
-for cfg, n in (('c4', 1 << 24), ('c2', 1 << 24)):
-    A = workloads.generate_torch(cfg, n, dev).double()
+for cfg, n in (('c2', 1 << 22), ('c3', 1 << 22), ('c4', 1 << 22)):
+    A = torch.as_tensor(workloads.generate(cfg, n)).to(dev).double()
     lam = torch.empty((n, 3), dtype=torch.float64, device=dev); ang = torch.empty_like(lam)
     st = torch.empty((n,), dtype=torch.uint8, device=dev)
     sd._lib.call("sd_eig3_classify_f64", A.data_ptr(), n, lam.data_ptr(), ang.data_ptr(), st.data_ptr(), torch.cuda.current_stream().cuda_stream)
