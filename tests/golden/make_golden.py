@@ -19,6 +19,9 @@ Sets (prefixes of the benchmark configs are exact, see workloads.py):
   eig2_c1    2x2 edge cases + first 4096 rows of config 1 (seed 0)
   stages_*   char_coeffs / compute_pq / eigenvalues3 / pq_expanded /
              compute_v / compute_w on the edge + c3 sets
+  signs_*    resolve_signs on the reference's own (lam, v, w) and
+             degenerate_double on its _double_root_lambdas, edge / c2 / c3 /
+             adversarial sets (`python make_golden.py signs` writes only these)
 """
 
 from __future__ import annotations
@@ -43,10 +46,8 @@ def save(name, **arrays):
     print(f"wrote {name}.npz", {k: v.shape for k, v in arrays.items()})
 
 
-def main():
-    if not refrun.available():
-        raise SystemExit("reference not available at " + refrun.REF_SRC)
-    sets3 = {
+def sets3_inputs():
+    return {
         "edge": cases.edge_cases_3x3(),
         "c2": workloads.generate("c2", 2048),
         "c3": workloads.generate("c3", 4096),
@@ -54,6 +55,23 @@ def main():
         "u11": np.random.default_rng(101).uniform(-1.0, 1.0, (2048, 6)),
         "adv": cases.adversarial_3x3(4096),
     }
+
+
+def sign_stages(sets3):
+    for name in ("edge", "c2", "c3", "adv"):
+        A = np.asarray(sets3[name], dtype=np.float64)
+        s = refrun.run_stages(A)
+        out = refrun.run_sign_stages(A, s["lam"], s["vw"])
+        save(f"signs_{name}", A=A, lam=s["lam"], vw=s["vw"], **out)
+
+
+def main(only=None):
+    if not refrun.available():
+        raise SystemExit("reference not available at " + refrun.REF_SRC)
+    sets3 = sets3_inputs()
+    if only == "signs":
+        sign_stages(sets3)
+        return
     for name, A in sets3.items():
         A32 = A if A.dtype == np.float32 else None
         A64 = np.asarray(A, dtype=np.float64)
@@ -70,6 +88,7 @@ def main():
         A = sets3[name]
         s = refrun.run_stages(A)
         save(f"stages_{name}", A=A, **s)
+    sign_stages(sets3)
     # oracle.py referees: Jacobi, cubic roots, residuals
     ref3 = np.concatenate([cases.edge_cases_3x3(), workloads.generate("c2", 1024),
                            workloads.generate("c3", 1024)])
@@ -104,4 +123,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

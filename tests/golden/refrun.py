@@ -284,3 +284,59 @@ def run_stages(A: np.ndarray):
     return dict(bcd=bcd, cc_status=cc_status, pqd=pqd, pq_status=pq_status,
                 lam=lam, pqe=pqe, pqe_status=pqe_status, vw=vw,
                 vw_status=vw_status)
+
+
+def _angles_record(i, angles, report, ang, status, rep):
+    ang[i] = angles.as_tuple()
+    s2, s3 = report.selected_signs
+    st = 0
+    if s2 < 0:
+        st |= S2_NEG
+    if s3 < 0:
+        st |= S3_NEG
+    if report.near_tie:
+        st |= NEAR_TIE
+    status[i] = st
+    rep[i, 0] = report.f1_norm
+    rep[i, 1] = report.f2_norm
+    rep[i, 3] = len(report.phi1_candidates)
+    for k, c in enumerate(report.phi1_candidates):
+        rep[i, 4 + 5 * k: 9 + 5 * k] = c
+
+
+def run_sign_stages(A: np.ndarray, lam: np.ndarray, vw: np.ndarray):
+    """resolve_signs (eig3.py:269-386) on the rows whose (lam, v, w) are
+    given (finite vw), and degenerate_double (eig3.py:389-454) on
+    (lam, lam3) = _double_root_lambdas(lam) (eig3.py:492-501) for every row
+    with finite lam.  Angles, status (sign / near-tie flags or the
+    exception's code), report rows (f-norms, candidate tuples; the residual
+    slot stays NaN, these stages do not compute it)."""
+    symdiag, eig3, core = _import()
+    A = np.asarray(A, dtype=np.float64).reshape(-1, 6)
+    n = A.shape[0]
+    out = {}
+    for tag in ("rs", "dd"):
+        out[f"{tag}_ang"] = np.full((n, 3), np.nan)
+        out[f"{tag}_status"] = np.full(n, 255, np.uint8)  # 255: stage not run on this row
+        out[f"{tag}_report"] = np.full((n, REPORT_STRIDE), np.nan)
+        out[f"{tag}_report"][:, 3] = 0.0
+    lam2 = np.full((n, 2), np.nan)
+    for i in range(n):
+        if not np.all(np.isfinite(lam[i])):
+            continue
+        m = sym3_from_packed(symdiag, A[i])
+        lams = tuple(float(x) for x in lam[i])
+        if np.all(np.isfinite(vw[i])):
+            try:
+                angles, report = eig3.resolve_signs(m, lams, float(vw[i, 0]), float(vw[i, 1]))
+                _angles_record(i, angles, report, out["rs_ang"], out["rs_status"], out["rs_report"])
+            except Exception as e:  # noqa: BLE001 — mapped to status codes
+                out["rs_status"][i] = exc_code(e)
+        lam2[i] = eig3._double_root_lambdas(lams)
+        try:
+            angles, report = eig3.degenerate_double(m, float(lam2[i, 0]), float(lam2[i, 1]))
+            _angles_record(i, angles, report, out["dd_ang"], out["dd_status"], out["dd_report"])
+        except Exception as e:  # noqa: BLE001
+            out["dd_status"][i] = exc_code(e)
+    out["lam2"] = lam2
+    return out

@@ -295,6 +295,57 @@ def test_stage_kernels_match_reference(name):
     st = st.cpu().numpy()
     vst = g["vw_status"][ok2]
     assert np.array_equal(st[st != 0], vst[st != 0])
+    # compute_w (eig3.py:198-206) on the reference's own v
+    okv = np.isfinite(g["vw"][ok2][:, 0])
+    vref = g["vw"][ok2][okv]
+    w, st = sd.compute_w_batched(torch.as_tensor(g["A"][ok2][okv]).to(DEV),
+                                 torch.as_tensor(g["lam"][ok2][okv]).to(DEV),
+                                 torch.as_tensor(vref[:, 0].copy()).to(DEV))
+    assert np.array_equal(st.cpu().numpy(), np.zeros(okv.sum(), np.uint8))
+    assert np.array_equal(w.cpu().numpy(), vref[:, 1])
+
+
+def _edge_window(ang):
+    """|phi2| or |phi3| within 1e-2 of 0 or pi/2: arccos(sqrt(.)) amplifies
+    1-ulp libm differences there."""
+    m = np.abs(ang[:, 1:3])
+    return ((m < 1e-2) | (np.abs(m - np.pi / 2) < 1e-2)).any(axis=1)
+
+
+@pytest.mark.parametrize("name", ["edge", "c2", "c3", "adv"])
+def test_sign_stage_kernels_match_reference_golden(name):
+    """resolve_signs (eig3.py:269-386) and degenerate_double (eig3.py:389-454)
+    as stage kernels, fed the reference's own (lam, v, w) / (lam, lam3):
+    identical status bytes (selected signs, near_tie, exception codes),
+    bit-identical f-norms (CPython hypot restated), identical candidate
+    availability, angles and candidates within 1e-10 mod pi (1e-7 in the
+    edge window)."""
+    g = load_golden(f"signs_{name}")
+    for tag, fn, args in (("rs", sd.resolve_signs_batched, ("lam", "vw")),
+                          ("dd", sd.degenerate_double_batched, ("lam2",))):
+        rows = np.nonzero(g[f"{tag}_status"] != 255)[0]
+        ins = [torch.as_tensor(np.ascontiguousarray(g[k][rows])).to(DEV) for k in ("A",) + args]
+        ang, st, rep = (x.cpu().numpy() for x in fn(*ins))
+        want = g[f"{tag}_status"][rows]
+        assert np.array_equal(st, want), (tag, np.nonzero(st != want)[0][:10])
+        ok = want < 8
+        ra, gr = g[f"{tag}_ang"][rows][ok], g[f"{tag}_report"][rows][ok]
+        ang, rep = ang[ok], rep[ok]
+        assert np.array_equal(rep[:, :2].view(np.uint64), gr[:, :2].view(np.uint64)), tag
+        assert np.array_equal(rep[:, 3], gr[:, 3]), tag
+        cand = np.arange(4, 24).reshape(4, 5)
+        assert np.array_equal(np.isnan(rep[:, 4:24]), np.isnan(gr[:, 4:24])), tag
+        assert np.array_equal(rep[:, cand[:, :2]], gr[:, cand[:, :2]], equal_nan=True), tag
+        edge = _edge_window(ra)
+        tol = np.where(edge, 1e-7, 1e-10)
+        err = np.nan_to_num(wrapped_diff(ang, ra)).max(axis=1)
+        assert np.all(err <= tol), (tag, float(err.max()), np.nonzero(err > tol)[0][:10])
+        cerr = np.nan_to_num(wrapped_diff(rep[:, cand[:, 2:4]], gr[:, cand[:, 2:4]]))
+        cerr = cerr.reshape(len(cerr), -1).max(axis=1)
+        assert np.all(cerr <= tol), (tag, float(cerr.max()))
+        dump(f"signs_{name}_{tag}", dict(rows=int(rows.size), ang_max=float(err.max(initial=0)),
+                                           cand_max=float(cerr.max(initial=0)),
+                                           ang_bit_equal=float(np.mean(np.all(ang == ra, axis=1)))))
 
 
 def test_device_glibc_pow_bit_exact():

@@ -84,6 +84,36 @@ def test_oracle_stages_match_golden(name):
     assert bits_equal(vw, g["vw"][ok2]).all()
 
 
+SIGN_SETS = ["edge", "c2", "c3", "adv"]
+
+
+def check_sign_stage(g, tag, ang, st, rep, rows):
+    """Status byte (sign / near-tie flags or exception code), the three
+    angles and every report field the stage fills (f-norms, the candidate
+    tuples), bit for bit on `rows`."""
+    want_st = g[f"{tag}_status"][rows]
+    assert np.array_equal(st, want_st), np.nonzero(st != want_st)[0][:10]
+    ok = want_st < 8
+    assert bits_equal(ang[ok], g[f"{tag}_ang"][rows][ok]).all()
+    keep = np.r_[0, 1, 3:24]
+    assert bits_equal(rep[ok][:, keep], g[f"{tag}_report"][rows][ok][:, keep]).all()
+
+
+@pytest.mark.parametrize("name", SIGN_SETS)
+def test_oracle_sign_stages_match_golden(name):
+    """resolve_signs (eig3.py:269-386) and degenerate_double (eig3.py:389-454)
+    called directly with the reference's own stage inputs."""
+    g = load_golden(f"signs_{name}")
+    rs = np.nonzero(g["rs_status"] != 255)[0]
+    assert rs.size > 0
+    ang, st, rep = O.resolve_signs(g["A"][rs], g["lam"][rs], g["vw"][rs])
+    check_sign_stage(g, "rs", ang, st, rep, rs)
+    dd = np.nonzero(g["dd_status"] != 255)[0]
+    assert dd.size > 0
+    ang, st, rep = O.degenerate_double(g["A"][dd], g["lam2"][dd])
+    check_sign_stage(g, "dd", ang, st, rep, dd)
+
+
 def test_py_hypot_is_cpython_hypot():
     rng = np.random.default_rng(11)
     for scale in (1.0, 1e-300, 1e300, 1e-160):
