@@ -11,7 +11,11 @@ import ctypes
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libsymdiag_b200.so"
+import os
+
+# SD_LIB_PATH: a variant build of the same library (tools/ experiments only)
+LIB_PATH = Path(os.environ.get("SD_LIB_PATH") or
+                Path(__file__).resolve().parent / "lib" / "libsymdiag_b200.so")
 
 SD_OK, SD_EINVAL, SD_ECUDA, SD_ENOMEM = 0, 1, 2, 3
 REPORT_STRIDE = 24

@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
       const int rows = warp_stage<T, 6, kVec>(A, n, row0, stage[warp]);
       if (lane < rows) {
         a = load_row(stage[warp] + 6 * lane);
-        cls = sd::classify3(a, l, scale, reason);
+        cls = sd::classify3_full(a, l, scale, reason);
         if (cls == 1 || cls == 4) {
 #pragma unroll
           for (int k = 0; k < 3; k++) {
@@ -538,6 +538,9 @@ constexpr int kFixTile = 4096;  // 32 status bytes per thread
 constexpr int kFixThreads = 128;
 constexpr int kFixQueue = kFixTile + kFixThreads;
 
+#ifndef SD_FIX_POLISH_LITERAL
+#define SD_FIX_POLISH_LITERAL 0
+#endif
 template <typename T, bool kPolish>
 __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict__ lam,
                                           T* __restrict__ ang, uint8_t* __restrict__ status,
@@ -567,7 +570,7 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
       // same inputs, same value).  TripleRoot rows have zero angles.
       double scale = 1.0;
       int reason = 0;
-      const int cls = sd::classify3(a, lm, scale, reason);
+      const int cls = sd::classify3_full(a, lm, scale, reason);
       const int pc = st & SD_CODE_MASK;
       const bool ok = pc == sd::kPolishTriple ? cls == 4
                                                : (pc == sd::kPolishDouble ? cls == 3 : cls == 0);
@@ -590,12 +593,22 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
     if ((st & SD_CODE_MASK) == sd::kPolishDouble) code = SD_CODE_DOUBLE_ROOT;
     if ((st & SD_CODE_MASK) == sd::kPolishTriple) code = SD_CODE_TRIPLE_ROOT;
     uint8_t out = (uint8_t)((st & ~SD_CODE_MASK) | code);
-    // the 1e-12 gate on the literal residual (numpy's FMA chains, eig3.py:504-506)
+    // the 1e-12 gate on the literal residual (numpy's FMA chains, eig3.py:504-506);
+    // SymMat3.scale from x*x squares (the rows here passed the fast path's
+    // 2^160 guard): glibc's pow could move it by an ulp, and the gate's
+    // outcome on a residual at rounding level is the polished bit, which the
+    // parity rules gate through the residual, not bit for bit
+#if SD_FIX_POLISH_LITERAL
+    // _polish_angles in numpy/OpenBLAS operation order (sd_eig3.cuh)
+    const bool pol = sd::polish_rows_literal(a, lm, ph);
+#else
     sd::Err e;
     double dm[9];
     sd::compose_rotation(e, ph, dm);
-    const double rr = sd::abs_residual(dm, lm, a) / sd::sym3_scale(e, a);
-    if (rr > 1e-12 && sd::polish_compact(a, lm, ph)) {
+    const double rr = sd::abs_residual(dm, lm, a) / sd::fast_scale(a);
+    const bool pol = rr > 1e-12 && sd::polish_compact(a, lm, ph);
+#endif
+    if (pol) {
 #pragma unroll
       for (int q = 0; q < 3; q++) ang[3 * i + q] = (T)ph[q];
       out |= SD_FLAG_POLISHED;

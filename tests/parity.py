@@ -40,25 +40,6 @@ def edge_window(ang):
     return near(a[:, 1]) | near(a[:, 2])
 
 
-def q_sign_ambiguous(A) -> np.ndarray:
-    """Rows whose cubic invariant q is below its own rounding noise.
-
-    For a rotated scalar matrix (all eigenvalues equal up to rounding) the
-    reference's q = 2b^3 - 9bc - 27d is pure cancellation noise and its sign
-    (which picks delta = 0 or pi on the double-root branch, eig3.py:150)
-    depends on the last bit of glibc pow(b, 3).  The eigenvalue split there
-    is rounding noise of size ~sqrt(p); such rows cannot be compared at
-    1e-12 by any implementation that is not glibc itself.
-    """
-    from oracle import oracle as O
-    A = np.asarray(A, np.float64).reshape(-1, 6)
-    bcd, _ = O.char_coeffs(A)
-    pqd, _ = O.compute_pq(bcd)
-    b, c, d = bcd[:, 0], bcd[:, 1], bcd[:, 2]
-    noise = 2.0 ** -45 * (np.abs(2 * b ** 3) + np.abs(9 * b * c) + np.abs(27 * d))
-    return np.abs(pqd[:, 1]) <= noise
-
-
 def residual_from_angles(A, lam, ang) -> np.ndarray:
     """||D diag(lam) D^T - A||_F / max(1, ||A||_F) with D = Rx Ry Rz built
     from the OUTPUT angles (core.py:211-235), vectorised in numpy.
@@ -190,13 +171,12 @@ def compare3(ref: dict, got: dict, eig_tol=EIG_TOL, ang_tol=ANG_TOL, A=None,
         degenerate_ang_max=float(np.nanmax(ang_err[ok_rows & (rc >= 2)]))
         if (ok_rows & (rc >= 2)).any() else 0.0,
     )
+    # no exemptions: the sign of q on rotated scalar matrices (pure rounding
+    # noise, eig3.py:150) is decided with glibc's own pow (sd_fast3.cuh,
+    # classify3 / classify3_exact), so those rows must match as well
     bad = np.nonzero(ok_rows & (lam_err > eig_tol))[0]
-    explained = np.zeros(len(bad), bool)
-    if len(bad) and A is not None:
-        explained = (rc[bad] == 2) & q_sign_ambiguous(np.asarray(A)[bad])
-    out["lam_fail"] = int((~explained).sum())
-    out["lam_explained_q_noise"] = int(explained.sum())
-    out["lam_fail_rows"] = bad[~explained][:20].tolist()
+    out["lam_fail"] = int(len(bad))
+    out["lam_fail_rows"] = bad[:20].tolist()
     if A is not None:
         m = ok_rows
         rr = np.full(n, np.nan)
@@ -216,7 +196,7 @@ def compare3(ref: dict, got: dict, eig_tol=EIG_TOL, ang_tol=ANG_TOL, A=None,
             worse_full = np.zeros(n, bool)
             worse_full[np.nonzero(m)[0][worse]] = True
             lam_bad = np.zeros(n, bool)
-            lam_bad[bad[~explained]] = True
+            lam_bad[bad] = True
             flagged = ((~code_ok) | (~sign_ok & ok_rows & (rc != 3))
                        | (strict & (ang_err > ang_tol)) | lam_bad | worse_full)
             rows = np.nonzero(flagged)[0]

@@ -113,12 +113,11 @@ def test_eig3_matches_oracle_large_prefix(config, n):
     A = workloads.generate(config, n).astype(np.float64)
     ref = O.eig3(A, report=True, nthreads=O.default_threads())
     got = gpu3(A)
-    stats = compare3(ref, got, A=A)
+    stats = compare3(ref, got, A=A, explain=True)
     dump(f"oracle_{config}_{n}", stats)
-    # a handful of rows may sit within rounding distance of a branch or sign
-    # threshold; they must be rare and each must be explained (test below)
-    assert_parity(stats, max_code=max(2, n // 100000), max_sign=max(2, n // 100000),
-                  max_strict_fail=max(2, n // 50000))
+    # every disagreement must be one the reference itself makes under 1-ulp
+    # libm perturbations (tests/parity.py), none unexplained
+    assert_parity(stats)
 
 
 def test_adversarial_rows_match_oracle():
@@ -151,15 +150,16 @@ def test_fast_path_matches_literal_path(config):
     got = dict(lam=fast.lam.cpu().numpy(), ang=fast.ang.cpu().numpy(),
                status=fast.status.cpu().numpy())
     assert not np.any((got["status"] & 0x0F) == 4), "deferred marker leaked"
-    stats = compare3(lit, got, A=A.cpu().numpy())
+    stats = compare3(lit, got, A=A.cpu().numpy(), explain=True)
     dump(f"fast_vs_literal_{config}", stats)
-    assert_parity(stats, max_code=2, max_sign=2, max_strict_fail=max(2, n // 50000))
+    assert_parity(stats)
 
 
 def test_eig3_f32_matches_reference_within_1e5():
     g = load_golden("eig3_c4")
     got = gpu3(g["A32"], report=False, dtype=torch.float32)
-    assert np.array_equal(got["status"] & 0x0F, g["status"] & 0x0F)
+    # branch codes and selected signs (fp32 storage, fp64 internals)
+    assert np.array_equal(got["status"] & 0x3F, g["status"] & 0x3F)
     lam_r = g["lam"]
     rel = np.abs(got["lam"] - lam_r) / np.abs(lam_r)
     assert rel.max() <= 1e-5
@@ -171,9 +171,9 @@ def test_eig3_f32_large_matches_oracle():
     A32 = workloads.generate("c4", 1 << 17)
     ref = O.eig3_f32(A32, nthreads=O.default_threads())
     got = gpu3(A32, report=False, dtype=torch.float32)
-    code_mis = ((ref["status"] ^ got["status"]) & 0x0F) != 0
-    assert code_mis.sum() <= 2
-    ok = ~code_mis & ((ref["status"] & 0x0F) < 8)
+    dec_mis = ((ref["status"] ^ got["status"]) & 0x3F) != 0  # branch code and signs
+    assert dec_mis.sum() == 0, np.nonzero(dec_mis)[0][:10]
+    ok = (ref["status"] & 0x0F) < 8
     rel = np.abs(got["lam"][ok].astype(np.float64) - ref["lam"][ok]) / np.abs(ref["lam"][ok])
     assert rel.max() <= 1e-5
 
@@ -327,8 +327,21 @@ def test_sign_stage_kernels_match_reference_golden(name):
         ins = [torch.as_tensor(np.ascontiguousarray(g[k][rows])).to(DEV) for k in ("A",) + args]
         ang, st, rep = (x.cpu().numpy() for x in fn(*ins))
         want = g[f"{tag}_status"][rows]
-        assert np.array_equal(st, want), (tag, np.nonzero(st != want)[0][:10])
-        ok = want < 8
+        mis = st != want
+        if name == "adv":
+            # the adversarial set puts phi1 exactly on the +-pi/2 wrap where
+            # _assemble_angles flips both signs (eig3.py:262-263): the last
+            # bit of atan2 picks one of two equivalent decompositions there.
+            # Only those rows may differ, and only in the sign flags.
+            ra = g[f"{tag}_ang"][rows]
+            boundary = np.abs(np.abs(ra[:, 0]) - np.pi / 2) < 1e-12
+            assert np.all(boundary[mis]), (tag, np.nonzero(mis & ~boundary)[0][:10])
+            assert np.all(((st ^ want)[mis] & 0x0F) == 0)
+            mis_rows = np.nonzero(mis)[0]
+        else:
+            assert not mis.any(), (tag, np.nonzero(mis)[0][:10])
+            mis_rows = np.zeros(0, int)
+        ok = (want < 8) & ~mis
         ra, gr = g[f"{tag}_ang"][rows][ok], g[f"{tag}_report"][rows][ok]
         ang, rep = ang[ok], rep[ok]
         assert np.array_equal(rep[:, :2].view(np.uint64), gr[:, :2].view(np.uint64)), tag
@@ -343,7 +356,8 @@ def test_sign_stage_kernels_match_reference_golden(name):
         cerr = np.nan_to_num(wrapped_diff(rep[:, cand[:, 2:4]], gr[:, cand[:, 2:4]]))
         cerr = cerr.reshape(len(cerr), -1).max(axis=1)
         assert np.all(cerr <= tol), (tag, float(cerr.max()))
-        dump(f"signs_{name}_{tag}", dict(rows=int(rows.size), ang_max=float(err.max(initial=0)),
+        dump(f"signs_{name}_{tag}", dict(rows=int(rows.size), wrap_flip_rows=int(mis_rows.size),
+                                           ang_max=float(err.max(initial=0)),
                                            cand_max=float(cerr.max(initial=0)),
                                            ang_bit_equal=float(np.mean(np.all(ang == ra, axis=1)))))
 
@@ -492,13 +506,13 @@ def test_c5_hbm_filling_batch(dtype):
     torch.cuda.empty_cache()
     if dtype == torch.float64:
         ref = O.eig3(As, report=True, nthreads=O.default_threads())
-        stats = compare3(ref, got, A=As)
-        assert_parity(stats, max_code=2, max_sign=2, max_strict_fail=2)
+        stats = compare3(ref, got, A=As, explain=True)
+        assert_parity(stats)
     else:
         ref = O.eig3_f32(As, nthreads=O.default_threads())
-        code_mis = ((ref["status"] ^ got["status"]) & 0x0F) != 0
-        assert code_mis.sum() <= 2
-        ok = ~code_mis & ((ref["status"] & 0x0F) < 8)
+        dec_mis = ((ref["status"] ^ got["status"]) & 0x3F) != 0  # branch code and signs
+        assert dec_mis.sum() <= 2
+        ok = ~dec_mis & ((ref["status"] & 0x0F) < 8)
         lr = ref["lam"][ok].astype(np.float64)
         norm = np.maximum(1.0, np.abs(lr).max(axis=1, keepdims=True))  # normwise
         assert (np.abs(got["lam"][ok] - lr) / norm).max() <= 1e-5
@@ -757,9 +771,9 @@ def test_fp32_mixed_batch_through_the_compaction_pass():
     A32 = workloads.generate("c3", 1 << 17).astype(np.float32)
     ref = O.eig3_f32(A32, nthreads=O.default_threads())
     got = gpu3(A32, dtype=torch.float32)
-    code_mis = ((ref["status"] ^ got["status"]) & 0x0F) != 0
-    assert code_mis.sum() <= 2
-    ok = ~code_mis & ((ref["status"] & 0x0F) < 8)
+    dec_mis = ((ref["status"] ^ got["status"]) & 0x3F) != 0  # branch code and signs
+    assert dec_mis.sum() == 0, np.nonzero(dec_mis)[0][:10]
+    ok = (ref["status"] & 0x0F) < 8
     lr = ref["lam"][ok].astype(np.float64)
     norm = np.maximum(1.0, np.abs(lr).max(axis=1, keepdims=True))
     assert (np.abs(got["lam"][ok] - lr) / norm).max() <= 1e-5
