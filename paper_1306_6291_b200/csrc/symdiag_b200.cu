@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
   __shared__ double ql[3][kFastSlots];
   __shared__ int qrow[kFastSlots];
   __shared__ int qgen, qdbl;  // generic rows fill the queue from the front, double roots from the back
+
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     qgen = 0;
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
       const int rows = warp_stage<T, 6, kVec>(A, n, row0, stage[warp]);
       if (lane < rows) {
         a = load_row(stage[warp] + 6 * lane);
-        cls = sd::classify3_full(a, l, scale, reason);
+        cls = sd::classify3(a, l, scale, reason);
         if (cls == 1 || cls == 4) {
 #pragma unroll
           for (int k = 0; k < 3; k++) {
@@ -305,6 +306,8 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
           status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT : sd::kPolishTriple;
         } else if (cls == 2) {
           status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
+        } else if (cls == sd::kClsExact) {
+          status[i] = sd::kExactPending;  // the exact pass (eig3_fixup_kernel<T, kFixExact>)
         }
       }
       __syncwarp();
@@ -519,17 +522,20 @@ __global__ void __launch_bounds__(kPassThreads, SD_PASS_MIN_BLOCKS)
   }
 }
 
-// Fix-up passes after the fast kernel:
-//   kPolish = true : rows marked kPolish* keep their closed-form result and
-//                    only run the Gauss-Newton tail (literal residual gate,
-//                    then polish_compact);
-//   kPolish = false: rows marked kDeferred are recomputed by the literal
-//                    solver (sd_eig3.cuh).
+// Fix-up passes after the fast kernel (and the compaction pass), in order:
+//   kFixExact  : rows marked kExactPending (classify3 could not certify a
+//                decision against glibc's pow) run classify3_exact and the
+//                fast bodies (exact_row);
+//   kFixPolish : rows marked kPolish* keep their closed-form result and
+//                only run the Gauss-Newton tail (literal residual gate,
+//                then polish_compact);
+//   kFixLiteral: rows marked kDeferred are recomputed by the literal
+//                solver (sd_eig3.cuh).
 // Such rows are sparse (0.02-10% of a batch) and each is expensive, so the
 // kernel is persistent: a grid of ~4 blocks per SM strides over tiles of
 // status bytes, queues the rows it owns in shared memory and runs them only
 // once a full block's worth has accumulated.  Dense warps, no tail of
-// one-row blocks, no global workspace.  Two separate launches keep each
+// one-row blocks, no global workspace.  Separate launches keep each
 // kernel's code small (the literal solver is ~13k SASS instructions).
 constexpr int kFixTile = 4096;  // 32 status bytes per thread
 #ifndef SD_FIX_MIN_BLOCKS
@@ -541,12 +547,59 @@ constexpr int kFixQueue = kFixTile + kFixThreads;
 #ifndef SD_FIX_POLISH_LITERAL
 #define SD_FIX_POLISH_LITERAL 0
 #endif
-template <typename T, bool kPolish>
+// kExactPending rows (classify3 could not certify a decision against
+// glibc's pow), in their own persistent pass between the compaction pass
+// and the polish pass: classify3_exact (glibc's pow for the powers the
+// gates could not certify), then the fast Generic / DoubleRoot bodies; a
+// closed form that needs the Gauss-Newton tail is written with its kPolish*
+// status for the polish pass, errors and threshold margins go to the
+// literal pass.  A pass of its own keeps this rarely run code (and glibc's
+// pow) out of the fast kernel, where it thrashed the instruction cache and
+// stalled blocks at the phase barrier (config 3: +0.4-0.9 ms).
+template <typename T>
+__device__ __forceinline__ void exact_row(const sd::Sym3& a, T* __restrict__ lam,
+                                          T* __restrict__ ang, uint8_t* __restrict__ status,
+                                          int64_t i) {
+  double l[3], phi[3] = {0.0, 0.0, 0.0}, xs = 1.0;
+  int reason = 0;
+  const int cls = sd::classify3_exact(a, l, xs, reason);
+  if (cls == 2) {  // errors and threshold margins: the literal solver
+    status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
+    return;
+  }
+  if (cls == 1 || cls == 4) {
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      lam[3 * i + q] = (T)l[q];
+      ang[3 * i + q] = (T)0.0;
+    }
+    // fp32 rows cannot carry a TripleRoot into the polish pass (it would
+    // recompute lambda with classify3): the literal solver takes them
+    status[i] = (cls == 1) ? SD_CODE_TRIPLE_ROOT
+                           : (sizeof(T) == 8 ? sd::kPolishTriple
+                                             : (uint8_t)(sd::kDeferred | (11 << 4)));
+    return;
+  }
+  uint8_t st = 0;
+  const double scale = sd::fast_scale(a);
+  const int rc = (cls == 0) ? sd::fast_generic(a, scale, l, phi, st)
+                            : sd::fast_double(a, scale, l, phi, st);
+  if (sizeof(T) != 8 && rc == sd::kFastPolish) {
+    status[i] = (uint8_t)(sd::kDeferred | (11 << 4));  // as above
+    return;
+  }
+  store_fast<T>(lam, ang, status, i, rc, l, phi, st);
+}
+
+constexpr int kFixLiteral = 0, kFixPolish = 1, kFixExact = 2;
+template <typename T, int kMode>
 __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict__ lam,
                                           T* __restrict__ ang, uint8_t* __restrict__ status,
                                           int64_t i) {
   const sd::Sym3 a = load_row(A + 6 * i);
-  if (!kPolish) {
+  if (kMode == kFixExact) {
+    exact_row<T>(a, lam, ang, status, i);
+  } else if (kMode == kFixLiteral) {
     sd::Result3<false> r;
     sd::diagonalize3<false>(a, r);
 #pragma unroll
@@ -570,7 +623,7 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
       // same inputs, same value).  TripleRoot rows have zero angles.
       double scale = 1.0;
       int reason = 0;
-      const int cls = sd::classify3_full(a, lm, scale, reason);
+      const int cls = sd::classify3(a, lm, scale, reason);
       const int pc = st & SD_CODE_MASK;
       const bool ok = pc == sd::kPolishTriple ? cls == 4
                                                : (pc == sd::kPolishDouble ? cls == 3 : cls == 0);
@@ -623,30 +676,35 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
 }
 
 // does a status byte belong to this pass?
-template <bool kPolish>
+template <int kMode>
 __device__ __forceinline__ bool fix_mine(unsigned byte) {
   const unsigned code = byte & SD_CODE_MASK;
-  return kPolish ? (code > sd::kDeferred && code < SD_ERR_FIRST)
-                 : (code == sd::kDeferred && byte != sd::kGenPending && byte != sd::kDblPending);
+  if (kMode == kFixExact) return byte == sd::kExactPending;
+  return kMode == kFixPolish
+             ? (code > sd::kDeferred && code < SD_ERR_FIRST)
+             : (code == sd::kDeferred && byte != sd::kGenPending && byte != sd::kDblPending &&
+                byte != sd::kExactPending);
 }
 
 // nonzero if any of the four status bytes in w belongs to this pass
-template <bool kPolish>
+template <int kMode>
 __device__ __forceinline__ unsigned fix_mine4(unsigned w) {
   const unsigned c = w & 0x0F0F0F0Fu;
-  if (kPolish) return __vcmpgeu4(c, 0x05050505u) & __vcmpleu4(c, 0x07070707u);
+  if (kMode == kFixExact) return __vcmpeq4(w, 0x01010101u * sd::kExactPending);
+  if (kMode == kFixPolish) return __vcmpgeu4(c, 0x05050505u) & __vcmpleu4(c, 0x07070707u);
   return __vcmpeq4(c, 0x04040404u) & ~__vcmpeq4(w, 0x01010101u * sd::kGenPending) &
-         ~__vcmpeq4(w, 0x01010101u * sd::kDblPending);
+         ~__vcmpeq4(w, 0x01010101u * sd::kDblPending) &
+         ~__vcmpeq4(w, 0x01010101u * sd::kExactPending);
 }
 
-// The literal pass (kPolish = false) runs the whole reference solver for a
+// The literal pass (kFixLiteral) runs the whole reference solver for a
 // few rows: SD_LIT_MIN_BLOCKS resident blocks (register cap vs spills; 2, 3,
 // 6, 8 measured no better than 4, profiles/r1_variants28_literal_blocks.jsonl).
 #ifndef SD_LIT_MIN_BLOCKS
 #define SD_LIT_MIN_BLOCKS SD_FIX_MIN_BLOCKS
 #endif
-template <typename T, bool kPolish>
-__global__ void __launch_bounds__(kFixThreads, kPolish ? SD_FIX_MIN_BLOCKS : SD_LIT_MIN_BLOCKS)
+template <typename T, int kMode>
+__global__ void __launch_bounds__(kFixThreads, kMode != kFixLiteral ? SD_FIX_MIN_BLOCKS : SD_LIT_MIN_BLOCKS)
     eig3_fixup_kernel(const T* __restrict__ A,
                                                                  int64_t n, T* __restrict__ lam,
                                                                  T* __restrict__ ang,
@@ -671,14 +729,14 @@ __global__ void __launch_bounds__(kFixThreads, kPolish ? SD_FIX_MIN_BLOCKS : SD_
       // four bytes per SIMD compare; the per-byte loop only on words that hit
 #pragma unroll
       for (int j = 0; j < 8; j++) {
-        if (!fix_mine4<kPolish>(words[j])) continue;
+        if (!fix_mine4<kMode>(words[j])) continue;
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          if (fix_mine<kPolish>((words[j] >> (8 * q)) & 0xffu)) mask |= 1u << (4 * j + q);
+          if (fix_mine<kMode>((words[j] >> (8 * q)) & 0xffu)) mask |= 1u << (4 * j + q);
       }
     } else {
       for (int q = 0; q < 32; q++)
-        if (r0 + q < n && fix_mine<kPolish>(status[r0 + q])) mask |= 1u << q;
+        if (r0 + q < n && fix_mine<kMode>(status[r0 + q])) mask |= 1u << q;
     }
     // tiles with no row for this pass skip the queue logic (one barrier)
     if (!__syncthreads_or(mask != 0u)) continue;
@@ -701,14 +759,14 @@ __global__ void __launch_bounds__(kFixThreads, kPolish ? SD_FIX_MIN_BLOCKS : SD_
     __syncthreads();
     const int c = cnt;
     if (c >= kFixThreads) {  // a full block's worth (or more): run them now
-      for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kPolish>(A, lam, ang, status, queue[k]);
+      for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kMode>(A, lam, ang, status, queue[k]);
       __syncthreads();
       if (tid == 0) cnt = 0;
     }
     __syncthreads();
   }
   const int c = cnt;
-  for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kPolish>(A, lam, ang, status, queue[k]);
+  for (int k = tid; k < c; k += kFixThreads) fixup_row<T, kMode>(A, lam, ang, status, queue[k]);
 }
 
 int fixup_grid(int64_t n, int blocks_per_sm) {
@@ -1332,10 +1390,14 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
     rc = check_launch("eig3_pass_kernel");
     if (rc != SD_OK) return rc;
   }
-  launch_after(eig3_fixup_kernel<T, true>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
+  launch_after(eig3_fixup_kernel<T, kFixExact>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
+  rc = check_launch("eig3_exact_kernel");
+  if (rc != SD_OK) return rc;
+  launch_after(eig3_fixup_kernel<T, kFixPolish>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;
-  launch_after(eig3_fixup_kernel<T, false>, g3, kFixThreads, s, A, n, lam, ang, status, vec);
+  launch_after(eig3_fixup_kernel<T, kFixLiteral>, g3, kFixThreads, s, A, n, lam, ang, status,
+               vec);
   return check_launch("eig3_literal_kernel");
 }
 
