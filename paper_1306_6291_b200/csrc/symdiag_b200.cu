@@ -1057,6 +1057,38 @@ __global__ void __launch_bounds__(kEig2Threads) eig2_bulk_kernel(
   }
 }
 
+// pair: each thread owns two ADJACENT rows (48 bytes), read as three 16-byte
+// loads when A is 16-byte aligned, computed as interleaved
+// branch-free chains like eig2_rows
+template <bool kVec, bool kReport>
+__global__ void __launch_bounds__(kEig2Threads, SD_EIG2_MIN_BLOCKS)
+    eig2_pair_kernel(const double* __restrict__ A, int64_t n, double* __restrict__ lam,
+                     double* __restrict__ phi, uint8_t* __restrict__ status,
+                     double* __restrict__ dmat) {
+  const int64_t i0 = 2 * ((int64_t)blockIdx.x * kEig2Threads + threadIdx.x);
+  if (i0 >= n) return;
+  double a[2][3];
+  if (i0 + 1 < n) {
+    const double2* src = reinterpret_cast<const double2*>(A + 3 * i0);
+    const double2 x = __ldg(src), y = __ldg(src + 1), z = __ldg(src + 2);
+    a[0][0] = x.x, a[0][1] = x.y, a[0][2] = y.x;
+    a[1][0] = y.y, a[1][1] = z.x, a[1][2] = z.y;
+  } else {
+    a[0][0] = __ldg(A + 3 * i0), a[0][1] = __ldg(A + 3 * i0 + 1), a[0][2] = __ldg(A + 3 * i0 + 2);
+    a[1][0] = a[1][1] = a[1][2] = 0.0;
+  }
+  double l1[2], l2[2], ph[2];
+  bool ok[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    ok[k] = !SD_EIG2_LITERAL && sd::diagonalize2_fast(a[k][0], a[k][1], a[k][2], l1[k], l2[k], ph[k]);
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if (i0 + k < n)
+      eig2_store<kVec, kReport>(i0 + k, ok[k], a[k][0], a[k][1], a[k][2], l1[k], l2[k], ph[k], lam,
+                                phi, status, dmat);
+}
+
 // persistent grid: SD_EIG2_BLOCKS_PER_SM resident blocks per SM, fewer for
 // small batches
 unsigned eig2_grid_persistent(int64_t n) {
@@ -1408,7 +1440,14 @@ int launch_eig2(const double* A, int64_t n, double* lam, double* phi, uint8_t* s
     return set_err(SD_EINVAL, "sd_eig2: bad argument");
   if (n == 0) return SD_OK;
   const bool vec = aligned(lam, 16);
-  if (SD_EIG2_MODE == 2 && aligned(A, 16)) {
+  if (SD_EIG2_MODE == 3 && aligned(A, 16)) {
+    const int64_t tile = (int64_t)kEig2Threads * 2;
+    const unsigned g = (unsigned)((n + tile - 1) / tile);
+    if (vec)
+      eig2_pair_kernel<true, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+    else
+      eig2_pair_kernel<false, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);
+  } else if (SD_EIG2_MODE == 2 && aligned(A, 16)) {
     const unsigned g = eig2_grid_persistent(n);
     if (vec)
       eig2_bulk_kernel<true, kReport><<<g, kEig2Threads, 0, s>>>(A, n, lam, phi, status, d);

@@ -29,16 +29,11 @@ VARIANTS = {
     "literal_r1_t128": {"SD_EIG2_LITERAL": 1, "SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1,
                         "SD_EIG2_THREADS": 128},
     "tile_r2_t128": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128},
-    "tile_r2_t128_mb12": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
-                          "SD_EIG2_MIN_BLOCKS": 12},
-    "tile_r2_t128_mb16": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
-                          "SD_EIG2_MIN_BLOCKS": 16},
-    "tile_r1_t128_mb12": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 128,
-                          "SD_EIG2_MIN_BLOCKS": 12},
-    "tile_r1_t128_mb16": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 128,
-                          "SD_EIG2_MIN_BLOCKS": 16},
-    "tile_r3_t128_mb10": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 3, "SD_EIG2_THREADS": 128,
-                          "SD_EIG2_MIN_BLOCKS": 10},
+    # round 2: adjacent row pairs read as three 16-byte loads (SD_EIG2_MODE 3)
+    "pair_t128": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 128},
+    "pair_t256": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 256},
+    "pair_t64": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 64},
+    "pair_t128_mb8": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 128, "SD_EIG2_MIN_BLOCKS": 8},
 }
 
 
