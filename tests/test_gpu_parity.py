@@ -120,6 +120,30 @@ def test_eig3_matches_oracle_large_prefix(config, n):
     assert_parity(stats)
 
 
+def test_rotated_scalar_rows_decide_like_glibc_pow():
+    """R diag(l, l, l) R^T in floating point: p = b^2 - 3c and q are pure
+    rounding noise, and the sign of q (the double-root endpoint, a ~sqrt(p)
+    eigenvalue split, eig3.py:147-150) is decided by the last bit of glibc's
+    pow(b, 3).  Round 1 exempted such rows as "q-noise"; with the device
+    restatement of glibc's pow (classify3 gates, classify3_exact) branch,
+    signs and eigenvalues must match the oracle on every row."""
+    from paper_1306_6291_b200.workloads import _quat_rotations
+    rng = np.random.default_rng(4242)
+    n = 1 << 17
+    R = _quat_rotations(rng.standard_normal((n, 4)))
+    lam = rng.uniform(-10.0, 10.0, n)
+    M = np.einsum("nij,nkj->nik", R * lam[:, None, None], R)
+    A = np.stack([M[:, 0, 0], M[:, 0, 1], M[:, 0, 2], M[:, 1, 1], M[:, 1, 2], M[:, 2, 2]], 1)
+    ref = O.eig3(A, report=True, nthreads=O.default_threads())
+    got = gpu3(A)
+    stats = compare3(ref, got, A=A, explain=True)
+    dump("oracle_rotated_scalar", stats)
+    assert (ref["status"] & 0x0F == 2).sum() > n // 20  # the q-noise population is there
+    assert stats["code_mismatch"] == 0 and stats["sign_mismatch"] == 0, stats
+    assert stats["lam_fail"] == 0, stats
+    assert_parity(stats)
+
+
 def test_adversarial_rows_match_oracle():
     """2^17 seeded rows on the decision boundaries (cases.adversarial_3x3):
     the fast path's guards must hand every ambiguous row to the literal path."""
