@@ -628,7 +628,9 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
   const double am[9] = {a.a11, a.a12, a.a13, a.a12, a.a22, a.a23, a.a13, a.a23, a.a33};
   auto recon = [&](const double* dd, double* r) {
     double dl[9], dt[9];
+#pragma unroll
     for (int i = 0; i < 3; i++)
+#pragma unroll
       for (int j = 0; j < 3; j++) {
         dl[3 * i + j] = dd[3 * i + j] * lam[j];
         dt[3 * i + j] = dd[3 * j + i];
@@ -637,6 +639,7 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
   };
   auto fro = [&](const double* r) {
     double s = 0.0;
+#pragma unroll
     for (int k = 0; k < 9; k++) {
       double x = r[k] - am[k];
       s = fma(x, x, s);
@@ -652,6 +655,7 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
   const double G1[9] = {0, 0, 0, 0, 0, -1, 0, 1, 0};
   const double G2[9] = {0, 0, 1, 0, 0, 0, -1, 0, 0};
   const double G3[9] = {0, -1, 0, 1, 0, 0, 0, 0, 0};
+#pragma unroll 1
   for (int it = 0; it < 2; it++) {
     double s1, c1, s2, c2;
     sincos(cur[0], &s1, &c1);
@@ -660,7 +664,9 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
     const double ry[9] = {c2, 0.0, s2, 0.0, 1.0, 0.0, -s2, 0.0, c2};
     double r12[9], r1t[9], r12t[9], t[9], g2[9], g3[9];
     mm3(r1, ry, r12);
+#pragma unroll
     for (int i = 0; i < 3; i++)
+#pragma unroll
       for (int j = 0; j < 3; j++) {
         r1t[3 * i + j] = r1[3 * j + i];
         r12t[3 * i + j] = r12[3 * j + i];
@@ -670,24 +676,31 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
     mm3(r12, G3, t);
     mm3(t, r12t, g3);
     double J[9][3];
+#pragma unroll
     for (int c = 0; c < 3; c++) {
       const double* g = c == 0 ? G1 : (c == 1 ? g2 : g3);
       double gr[9], rg[9];
       mm3(g, rec, gr);
       mm3(rec, g, rg);
+#pragma unroll
       for (int k = 0; k < 9; k++) J[k][c] = gr[k] - rg[k];
     }
     double jtj[9], jtr[3], x[3];
+#pragma unroll
     for (int i = 0; i < 3; i++)
+#pragma unroll
       for (int j = 0; j < 3; j++) {
         double s = J[0][i] * J[0][j];
+#pragma unroll
         for (int k = 1; k < 9; k++) s = fma(J[k][i], J[k][j], s);
         jtj[3 * i + j] = s + (i == j ? damp : 0.0);
       }
     double resid[9];
+#pragma unroll
     for (int k = 0; k < 9; k++) resid[k] = rec[k] - am[k];
     jt_resid_ob(J, resid, jtr);
     solve3_ob(jtj, jtr, x);
+#pragma unroll
     for (int i = 0; i < 3; i++) cur[i] = cur[i] - x[i];
     compose_rotation(e, cur, d);
     recon(d, rec);
