@@ -18,7 +18,9 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "build" / "libsymdiag_oracle.so"
+# SD_ORACLE_LIB selects another build of the same source (tools only, e.g.
+# build/libsymdiag_oracle_cr.so: the correctly rounded libm variant)
+LIB_PATH = Path(os.environ.get("SD_ORACLE_LIB", HERE / "build" / "libsymdiag_oracle.so"))
 REPORT_STRIDE = 24
 
 _lib = None
@@ -31,12 +33,29 @@ def build(force: bool = False) -> Path:
     return LIB_PATH
 
 
-def lib():
+CR_LIB_PATH = HERE / "build" / "libsymdiag_oracle_cr.so"
+_libs = {}
+
+
+def lib(path=None):
+    """The oracle library (glibc libm); `path` = another build of the same
+    source, e.g. CR_LIB_PATH (the correctly rounded libm variant)."""
     global _lib
+    if path is not None:
+        if path not in _libs:
+            if not Path(path).exists():
+                build(force=True)
+            _libs[path] = _bind(ctypes.CDLL(str(path)))
+        return _libs[path]
     if _lib is None:
         if not LIB_PATH.exists():
             build()
-        L = ctypes.CDLL(str(LIB_PATH))
+        _lib = _bind(ctypes.CDLL(str(LIB_PATH)))
+    return _lib
+
+
+def _bind(L):
+    if True:
         P = ctypes.c_void_p
         I64 = ctypes.c_int64
         L.sdo_eig3.argtypes = [P, I64, P, P, P, P, P, ctypes.c_int]
@@ -58,8 +77,7 @@ def lib():
         L.sdo_set_nudge.argtypes = [ctypes.c_int, ctypes.c_uint64]
         L.sdo_py_hypot.argtypes = [ctypes.c_double, ctypes.c_double]
         L.sdo_py_hypot.restype = ctypes.c_double
-        _lib = L
-    return _lib
+    return L
 
 
 def _p(a):
@@ -77,16 +95,19 @@ def default_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def eig3(A, nthreads: int = 1, report: bool = False, d: bool = False):
-    """diagonalize3 over packed A[n,6] -> dict(lam, ang, status[, report, d])."""
+def eig3(A, nthreads: int = 1, report: bool = False, d: bool = False, cr: bool = False):
+    """diagonalize3 over packed A[n,6] -> dict(lam, ang, status[, report, d]).
+    cr=True: the build with correctly rounded sin/cos/acos/asin/atan2/hypot
+    (oracle/cr_variant.c) -- the libm of the device's literal solver."""
     A = _c(A, width=6)
     n = A.shape[0]
     out = dict(lam=np.empty((n, 3)), ang=np.empty((n, 3)),
                status=np.empty(n, np.uint8))
     out["report"] = np.empty((n, REPORT_STRIDE)) if report else None
     out["d"] = np.empty((n, 9)) if d else None
-    lib().sdo_eig3(_p(A), n, _p(out["lam"]), _p(out["ang"]), _p(out["status"]),
-                   _p(out["report"]), _p(out["d"]), nthreads)
+    lib(CR_LIB_PATH if cr else None).sdo_eig3(
+        _p(A), n, _p(out["lam"]), _p(out["ang"]), _p(out["status"]),
+        _p(out["report"]), _p(out["d"]), nthreads)
     return out
 
 

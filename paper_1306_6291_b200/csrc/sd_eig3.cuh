@@ -658,8 +658,8 @@ __device__ __noinline__ double polish_angles(const Sym3& a, const double* lam, d
 #pragma unroll 1
   for (int it = 0; it < 2; it++) {
     double s1, c1, s2, c2;
-    sincos(cur[0], &s1, &c1);
-    sincos(cur[1], &s2, &c2);
+    lit_sincos(cur[0], &s1, &c1);
+    lit_sincos(cur[1], &s2, &c2);
     const double r1[9] = {1.0, 0.0, 0.0, 0.0, c1, -s1, 0.0, s1, c1};
     const double ry[9] = {c2, 0.0, s2, 0.0, 1.0, 0.0, -s2, 0.0, c2};
     double r12[9], r1t[9], r12t[9], t[9], g2[9], g3[9];
@@ -778,8 +778,8 @@ __device__ __forceinline__ void diagonalize3(const Sym3& a, Result3<kReport>& r)
       lam[0] = lam[1] = lam[2] = b / 3.0;
       ar.phi[0] = ar.phi[1] = ar.phi[2] = 0.0;
       if (kReport) {
-        ar.n1 = hypot(a.a12, -a.a13);
-        ar.n2 = hypot(a.a22 - a.a33, -2.0 * a.a23);
+        ar.n1 = lit_hypot(a.a12, -a.a13);
+        ar.n2 = lit_hypot(a.a22 - a.a33, -2.0 * a.a23);
       }
       code = SD_CODE_TRIPLE_ROOT;
     } else {

@@ -12,16 +12,27 @@
 //   math.hypot    -> CPython 3.12 vector_norm algorithm (exact restatement)
 //   math.remainder-> CUDA remainder (exact, as glibc)
 //   math.sqrt     -> IEEE sqrt (correctly rounded, as glibc)
-//   sin/cos/acos/asin/atan2 -> CUDA libdevice (<= 2 ulp vs glibc's < 1 ulp;
-//                    the resulting angle differences are what the parity
-//                    tolerance covers)
+//   sin/cos/acos/asin/atan2, numpy hypot -> correctly rounded
+//                    (sd_crlibm.h): glibc's own value except where glibc
+//                    misrounds (0.03-0.25% of arguments, ~0.51 ulp); the
+//                    fast path uses its own cheaper functions and bounds
+//                    or defers every decision they could move
 // CPython's exception rules for math.* / ** are mirrored as status codes.
 #pragma once
 
 #include <cstdint>
 
 #include "../../include/symdiag_b200.h"
+#include "sd_crlibm.h"
 #include "sd_glibc_pow.h"
+
+// SD_LIT_CRLIBM (on): the literal solver's sin/cos/acos/asin/atan2 and
+// numpy's hypot are correctly rounded (sd_crlibm.h) instead of libdevice's
+// 1-2 ulp versions, so its values and last-bit decisions are glibc's
+// wherever glibc is correctly rounded
+#ifndef SD_LIT_CRLIBM
+#define SD_LIT_CRLIBM 1
+#endif
 
 namespace sd {
 
@@ -96,12 +107,31 @@ __device__ __forceinline__ double chk(Err& e, double r, double x) {
   return r;
 }
 __device__ __forceinline__ double py_sqrt(Err& e, double x) { return chk(e, sqrt(x), x); }
-__device__ __forceinline__ double py_acos(Err& e, double x) { return chk(e, acos(x), x); }
-__device__ __forceinline__ double py_asin(Err& e, double x) { return chk(e, asin(x), x); }
-__device__ __forceinline__ double py_sin(Err& e, double x) { return chk(e, sin(x), x); }
-__device__ __forceinline__ double py_cos(Err& e, double x) { return chk(e, cos(x), x); }
+#if SD_LIT_CRLIBM
+// correctly rounded (sd_crlibm.h): equal to glibc's wherever glibc rounds
+// correctly (99.75-99.97% of arguments), one out-of-line copy each
+__device__ __noinline__ double lit_acos(double x) { return sdcr_acos(x); }
+__device__ __noinline__ double lit_asin(double x) { return sdcr_asin(x); }
+__device__ __noinline__ void lit_sincos(double x, double* s, double* c) { sdcr_sincos(x, s, c); }
+__device__ __noinline__ double lit_sin(double x) { return sdcr_sin(x); }
+__device__ __noinline__ double lit_cos(double x) { return sdcr_cos(x); }
+__device__ __noinline__ double lit_atan2(double y, double x) { return sdcr_atan2(y, x); }
+__device__ __noinline__ double lit_hypot(double x, double y) { return sdcr_hypot(x, y); }
+#else
+__device__ __forceinline__ double lit_acos(double x) { return acos(x); }
+__device__ __forceinline__ double lit_asin(double x) { return asin(x); }
+__device__ __forceinline__ void lit_sincos(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ double lit_sin(double x) { return sin(x); }
+__device__ __forceinline__ double lit_cos(double x) { return cos(x); }
+__device__ __forceinline__ double lit_atan2(double y, double x) { return atan2(y, x); }
+__device__ __forceinline__ double lit_hypot(double x, double y) { return hypot(x, y); }
+#endif
+__device__ __forceinline__ double py_acos(Err& e, double x) { return chk(e, lit_acos(x), x); }
+__device__ __forceinline__ double py_asin(Err& e, double x) { return chk(e, lit_asin(x), x); }
+__device__ __forceinline__ double py_sin(Err& e, double x) { return chk(e, lit_sin(x), x); }
+__device__ __forceinline__ double py_cos(Err& e, double x) { return chk(e, lit_cos(x), x); }
 __device__ __forceinline__ void py_sincos(Err& e, double x, double* s, double* c) {
-  sincos(x, s, c);
+  lit_sincos(x, s, c);
   chk(e, *s, x);
 }
 
@@ -207,7 +237,7 @@ __device__ __forceinline__ double angle_of(Err& e, double x, double y) {
     e.raise(SD_ERR_ANGLE_OF_ZERO);
     return __longlong_as_double(0x7ff8000000000000LL);
   }
-  double r = atan2(y, x);
+  double r = lit_atan2(y, x);
   if (r == -kPi) r = kPi;
   return r;
 }

@@ -168,3 +168,45 @@ def edge_cases_2x2() -> np.ndarray:
         rows.append([a11, a12, a22])
         rows.append([a22, a12, a11])       # swap symmetry pair
     return np.array(rows, dtype=np.float64)
+
+
+def lastbit_3x3(n: int, seed: int = 7300) -> np.ndarray:
+    """Seeded rows whose reference decisions hinge on the last bits of
+    glibc's acos / cos / sin (round-2 sweeps: the two c3 DoubleRoot-vs-
+    Generic rows and the c4 phi3 sign row were all of these kinds):
+      - diagonal matrices with two entries at relative gaps 1e-4 .. 1e-1
+        (v is rounding noise of the eigenvalues: the V_ZERO_EPS test and
+        the w clamp decide DoubleRoot vs Generic, eig3.py:183-206, 547)
+      - the same with one tiny off-diagonal a23 (f1 = 0 route)
+      - random rotations with |phi3| or |phi2| at 1e-9 .. 1e-6 of 0 or
+        pi/2 (w, v within an ulp of 0 / 1: the sign selection of
+        eig3.py:302-326 on noise-sized magnitudes)
+      - random rotations of eigenvalues with relative gaps 1e-8 .. 1e-5
+        (conditioning: angles carry the eigenvalues' last-bit noise)
+    """
+    rng = np.random.default_rng(seed)
+    rows = np.empty((n, 6))
+    fam = rng.integers(0, 4, n)
+    for i in range(n):
+        f = fam[i]
+        if f in (0, 1):
+            x = rng.uniform(-5, 5)
+            d = [x, x * (1 + 10 ** rng.uniform(-4, -1) * rng.choice([-1, 1])), rng.uniform(-5, 5)]
+            rng.shuffle(d)
+            r = np.zeros(6)
+            r[[0, 3, 5]] = d
+            if f == 1:
+                r[4] = 10 ** rng.uniform(-12, -6) * rng.choice([-1, 1])
+            rows[i] = r
+        elif f == 2:
+            phis = list(rng.uniform(-math.pi / 2, math.pi / 2, 3))
+            k = rng.integers(1, 3)
+            t = 10 ** rng.uniform(-9, -6)
+            phis[k] = (t if rng.random() < 0.5 else math.pi / 2 - t) * rng.choice([-1, 1])
+            rows[i] = _conj(phis, rng.uniform(-4, 4, 3))
+        else:
+            base = rng.uniform(-5, 5)
+            lam = [base, base * (1 + 10 ** rng.uniform(-8, -5)), rng.uniform(-5, 5)]
+            q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+            rows[i] = _pack((q * np.asarray(lam)) @ q.T)
+    return rows

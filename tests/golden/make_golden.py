@@ -22,6 +22,10 @@ Sets (prefixes of the benchmark configs are exact, see workloads.py):
   signs_*    resolve_signs on the reference's own (lam, v, w) and
              degenerate_double on its _double_root_lambdas, edge / c2 / c3 /
              adversarial sets (`python make_golden.py signs` writes only these)
+  eig3_lastbit  rows whose decisions hinge on glibc's last bits:
+             cases.lastbit_3x3(4096) plus the rows the round-2 2^26 sweeps
+             flagged (profiles/r2/parity_sweep/*_flagged.npz: seeded c2/c3/c4
+             rows), `python make_golden.py lastbit` writes only this
 """
 
 from __future__ import annotations
@@ -65,9 +69,23 @@ def sign_stages(sets3):
         save(f"signs_{name}", A=A, lam=s["lam"], vw=s["vw"], **out)
 
 
+def lastbit():
+    rows = [cases.lastbit_3x3(4096)]
+    for c in ("c2", "c3", "c4"):
+        f = HERE.parents[1] / "profiles" / "r2" / "parity_sweep" / f"sweep_{c}_flagged.npz"
+        rows.append(np.load(f)["A"])
+    A = np.concatenate(rows).astype(np.float64)
+    r = refrun.run_eig3(A)
+    save("eig3_lastbit", A=A, lam=r["lam"], ang=r["ang"], status=r["status"],
+         report=r["report"])
+
+
 def main(only=None):
     if not refrun.available():
         raise SystemExit("reference not available at " + refrun.REF_SRC)
+    if only == "lastbit":
+        lastbit()
+        return
     sets3 = sets3_inputs()
     if only == "signs":
         sign_stages(sets3)
@@ -89,6 +107,7 @@ def main(only=None):
         s = refrun.run_stages(A)
         save(f"stages_{name}", A=A, **s)
     sign_stages(sets3)
+    lastbit()
     # oracle.py referees: Jacobi, cubic roots, residuals
     ref3 = np.concatenate([cases.edge_cases_3x3(), workloads.generate("c2", 1024),
                            workloads.generate("c3", 1024)])

@@ -156,6 +156,49 @@ def test_adversarial_rows_match_oracle():
     assert_parity(stats)
 
 
+def test_lastbit_rows_decide_like_the_reference():
+    """Rows whose reference decisions hinge on glibc's last bits
+    (tests/golden/eig3_lastbit: diagonal matrices with close entries,
+    |phi2|/|phi3| within 1e-9..1e-6 of 0 or pi/2, gaps 1e-8..1e-5, plus the
+    rows the round-2 2^26 sweeps flagged, incl. the two c3 DoubleRoot-vs-
+    Generic rows and the c4 phi3-sign row).  The fast path must defer every
+    such decision and the literal solver, with its correctly rounded libm
+    (sd_crlibm.h), must then take the reference's: branch, signs, near_tie
+    identical on every row, eigenvalues within 1e-12."""
+    g = load_golden("eig3_lastbit")
+    got = gpu3(g["A"])
+    stats = compare3(g, got, A=g["A"])
+    dump("golden_lastbit", stats)
+    bad = np.nonzero((got["status"] ^ g["status"]) & 0x7F)[0]
+    assert len(bad) == 0, [(int(i), hex(g["status"][i]), hex(got["status"][i])) for i in bad[:8]]
+    assert stats["lam_fail"] == 0, stats
+    assert_parity(stats)
+
+
+def test_lastbit_family_matches_cr_oracle_decisions():
+    """2^17 fresh last-bit rows (cases.lastbit_3x3, another seed): the GPU's
+    decisions equal, row for row, those of the oracle built with the same
+    correctly rounded libm (O.eig3(cr=True)) -- the fast path defers what it
+    cannot certify, the literal solver computes what the oracle computes --
+    and differ from the glibc oracle's only on rows where the two oracles
+    differ (a misrounded glibc call, ~2e-5 of this adversarial family)."""
+    from cases import lastbit_3x3
+    A = lastbit_3x3(1 << 17, seed=7301)
+    ref = O.eig3(A, nthreads=O.default_threads())
+    crr = O.eig3(A, nthreads=O.default_threads(), cr=True)
+    got = gpu3(A)
+    d_cr = np.nonzero((got["status"] ^ crr["status"]) & 0x7F)[0]
+    assert len(d_cr) == 0, [(int(i), hex(crr["status"][i]), hex(got["status"][i])) for i in d_cr[:8]]
+    d_ref = ((got["status"] ^ ref["status"]) & 0x7F) != 0
+    oracles_differ = ((crr["status"] ^ ref["status"]) & 0x7F) != 0
+    assert not (d_ref & ~oracles_differ).any()
+    dump("lastbit_family", {"n": int(len(A)), "gpu_vs_glibc_decisions": int(d_ref.sum()),
+                            "oracles_differ": int(oracles_differ.sum()),
+                            "gpu_vs_cr_decisions": int(len(d_cr)),
+                            "lam_bit_equal_vs_cr": float((got["lam"] == crr["lam"]).all(1).mean()),
+                            "lam_bit_equal_vs_glibc": float((got["lam"] == ref["lam"]).all(1).mean())})
+
+
 @pytest.mark.parametrize("config", ["c2", "c3", "c4"])
 def test_fast_path_matches_literal_path(config):
     """sd_eig3_f64 (fast path + deferred literal rows) vs sd_eig3_literal_f64

@@ -18,7 +18,7 @@ from conftest import bits_equal, load_golden, wrapped_diff
 from oracle import oracle as O
 
 POLISHED = 0x80
-SETS3 = ["edge", "c2", "c3", "c4", "u11", "adv"]
+SETS3 = ["edge", "c2", "c3", "c4", "u11", "adv", "lastbit"]
 
 
 def check_eig3_against(ref, got, A=None):
