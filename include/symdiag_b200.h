@@ -182,6 +182,17 @@ int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots,
 int sd_glibc_pow_f64(const double* x, const double* y, int64_t n, double* out,
                      void* cuda_stream);
 
+/* The literal solver's libm, elementwise: fn 0 sin(x), 1 cos(x), 2 acos(x),
+ * 3 asin(x), 4 atan2(x, y), 5 hypot(x, y) (y may be NULL for fn < 4),
+ * correctly rounded (csrc/sd_crlibm.h: a quick double-double phase with a
+ * rounding test, an accurate phase behind it), i.e. the value CPython's
+ * math.sin / cos / acos / asin / atan2 / hypot return on the reference's
+ * host wherever glibc itself rounds correctly.  Replaces the libm calls of
+ * eig3.py:143-174, 218-246, 288-379 and core.py:238-246 on the rows the
+ * literal pass solves.                                                       */
+int sd_crlibm_f64(int fn, const double* x, const double* y, int64_t n, double* out,
+                  void* cuda_stream);
+
 /* ---- host-buffer path (end-to-end: H2D, kernel, D2H, pipelined) ---------- */
 typedef struct sd_plan sd_plan;
 /* A plan owns three device staging slots of `chunk` matrices and three CUDA

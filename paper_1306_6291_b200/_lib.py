@@ -43,6 +43,7 @@ SIGNATURES = {
     "sd_residuals_f64": [_I, _P, _P, _P, _I64, _P, _P],
     "sd_cubic_roots_f64": [_P, _I64, _P, _P, _P],
     "sd_glibc_pow_f64": [_P, _P, _I64, _P, _P],
+    "sd_crlibm_f64": [_I, _P, _P, _I64, _P, _P],
     "sd_plan_create": [_I, _I64, ctypes.POINTER(_P)],
     "sd_eig3_report_f64_host": [_P, _P, _I64, _P, _P, _P, _P, _P],
     "sd_eig2_report_f64_host": [_P, _P, _I64, _P, _P, _P, _P],

@@ -387,6 +387,28 @@ def glibc_pow_batched(x: torch.Tensor, y) -> torch.Tensor:
     return out
 
 
+_CR_FN = {"sin": 0, "cos": 1, "acos": 2, "asin": 3, "atan2": 4, "hypot": 5}
+
+
+def crlibm_batched(fn: str, x: torch.Tensor, y: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The literal solver's correctly rounded libm, elementwise (csrc/sd_crlibm.h):
+    fn in sin, cos, acos, asin, atan2(x, y), hypot(x, y)."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64:
+        raise TypeError("x must be a CUDA float64 tensor")
+    code = _CR_FN[fn]
+    x = x.contiguous().view(-1)
+    if code >= 4:
+        if y is None:
+            raise ValueError(f"{fn} takes two arguments")
+        y = y.to(device=x.device, dtype=torch.float64).contiguous().view(-1)
+        _same_rows(x.shape[0], x.device, y)
+    out = torch.empty_like(x)
+    with torch.cuda.device(x.device):
+        _lib.call("sd_crlibm_f64", code, x.data_ptr(), _ptr(y) if code >= 4 else None,
+                  x.shape[0], out.data_ptr(), _stream())
+    return out
+
+
 class HostPlan:
     """End-to-end path over HOST buffers (numpy or pinned torch CPU tensors):
     chunked H2D -> kernel -> D2H, pipelined over three streams in C++

@@ -258,6 +258,20 @@ __device__ __forceinline__ void store_fast(T* lam, T* ang, uint8_t* status, int6
   status[r] = st;  // branch code, kPolish*, or kDeferred with its reason
 }
 
+// SD_FAST_SORT: the refinement windows of the Generic body (eig3.py:352-374)
+// are taken by about half the rows each (|phi2|, |phi3| below pi/8 or above
+// 3pi/8), so in a warp of arbitrary rows every window site runs for every
+// warp at ~50% of its lanes.  Sorting the block's Generic rows by window
+// class (4 classes in Gray order, from v and w) before the long part of
+// the body lets whole warps skip the sites none of their rows needs.
+// Measured (gpurun r2d, 2^24 rows, ncu durations of the fast kernel): c4
+// 1800 -> 1772 us, but c2 1806 -> 1827 us and c3 964 -> 1016 us — the two
+// extra barriers, the second reload of A and the queue rewrite cost about
+// what the skipped window sites save: off.
+#ifndef SD_FAST_SORT
+#define SD_FAST_SORT 0
+#endif
+
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     eig3_fast_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
@@ -276,12 +290,20 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
   __shared__ double ql[3][kFastSlots];
   __shared__ int qrow[kFastSlots];
   __shared__ int qgen, qdbl;  // generic rows fill the queue from the front, double roots from the back
+#if SD_FAST_SORT
+  constexpr bool kSorted = kFastRows == 1 && !kStoreA;
+  __shared__ double qv[kSorted ? kFastSlots : 1], qw[kSorted ? kFastSlots : 1];
+  __shared__ int qcls[4];
+#endif
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     qgen = 0;
     qdbl = 0;
   }
+#if SD_FAST_SORT
+  if (tid < 4) qcls[tid] = 0;
+#endif
   __syncthreads();
   const int64_t blk0 = (int64_t)blockIdx.x * kFastSlots;
 #pragma unroll 1
@@ -345,6 +367,82 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
   const int ng = qgen, nd = qdbl;
   const bool pass_gen = SD_PASS && ng < kPassMin * kFastRows;
   const bool pass_dbl = SD_PASS && nd < kPassMinDbl * kFastRows;
+#if SD_FAST_SORT
+  if (kSorted) {
+    // Window-class sort (see SD_FAST_SORT above): B1 computes v, w of this
+    // thread's Generic slot and its window class; a counting sort over the
+    // block's four classes regroups the rows (in place: every slot is read
+    // before the first barrier and rewritten after it); B2 runs the rest of
+    // the Generic body on class-homogeneous warps.  DoubleRoot rows take
+    // the threads behind the sorted Generic rows.
+    const bool run_gen = tid < ng && !pass_gen;
+    if (tid < ng && pass_gen) {
+      const int64_t r = blk0 + qrow[tid];
+      const double gl[3] = {ql[0][tid], ql[1][tid], ql[2][tid]};
+      stash_lam<T>(lam, ang, r, gl);
+      status[r] = sd::kGenPending;
+    }
+    int key = -1, rel = 0;
+    double gl[3] = {0.0, 0.0, 0.0}, v = 0.0, w = 0.0;
+    if (run_gen) {
+      rel = qrow[tid];
+      const int64_t r = blk0 + rel;
+      const sd::Sym3 g = load_row(A + 6 * r);
+      gl[0] = ql[0][tid], gl[1] = ql[1][tid], gl[2] = ql[2][tid];
+      uint8_t st = 0;
+      if (sd::generic_vw(g, gl, v, w, st) == sd::kFastDone)
+        key = sd::window_class(v, w);
+      else
+        status[r] = st;  // deferred with its reason: literal pass
+    }
+    int off = 0;
+    {
+      const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const unsigned m = __ballot_sync(0xffffffffu, key == k);
+        int b = 0;
+        if (lane == 0 && m) b = atomicAdd(&qcls[k], __popc(m));
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (key == k) off = b + __popc(m & below);
+      }
+    }
+    __syncthreads();
+    const int c0 = qcls[0], c1 = qcls[1], c2 = qcls[2], c3 = qcls[3];
+    if (key >= 0) {
+      const int s = off + (key > 0 ? c0 : 0) + (key > 1 ? c1 : 0) + (key > 2 ? c2 : 0);
+      ql[0][s] = gl[0], ql[1][s] = gl[1], ql[2][s] = gl[2];
+      qv[s] = v, qw[s] = w;
+      qrow[s] = rel;
+    }
+    __syncthreads();
+    const int nsorted = c0 + c1 + c2 + c3;
+    if (tid < nsorted) {
+      const int64_t r = blk0 + qrow[tid];
+      const sd::Sym3 g = load_row(A + 6 * r);
+      double l3[3] = {ql[0][tid], ql[1][tid], ql[2][tid]};
+      double phi[3];
+      uint8_t st = 0;
+      const int rc = sd::generic_rest(g, sd::fast_scale(g), l3, qv[tid], qw[tid], phi, st);
+      store_fast<T>(lam, ang, status, r, rc, l3, phi, st);
+    } else if (tid - nsorted < nd) {
+      const int slot = kFastSlots - 1 - (tid - nsorted);
+      const int64_t r = blk0 + qrow[slot];
+      double l3[3] = {ql[0][slot], ql[1][slot], ql[2][slot]};
+      if (pass_dbl) {
+        stash_lam<T>(lam, ang, r, l3);
+        status[r] = sd::kDblPending;
+      } else {
+        const sd::Sym3 g = load_row(A + 6 * r);
+        double phi[3];
+        uint8_t st = 0;
+        const int rc = sd::fast_double(g, sd::fast_scale(g), l3, phi, st);
+        store_fast<T>(lam, ang, status, r, rc, l3, phi, st);
+      }
+    }
+    return;
+  }
+#endif
 #pragma unroll 1
   for (int slot = tid; slot < kFastSlots; slot += kFastThreads) {
     const bool is_gen = slot < ng;
@@ -1362,6 +1460,24 @@ __global__ void glibc_pow_kernel(const double* x, const double* y, int64_t n, do
   if (i < n) out[i] = sd::glibc_pow(x[i], y[i]);
 }
 
+// the literal solver's libm (sd_crlibm.h through sd_math.cuh's lit_*):
+// fn 0 sin, 1 cos, 2 acos, 3 asin, 4 atan2(x, y), 5 hypot(x, y)
+__global__ void crlibm_kernel(int fn, const double* x, const double* y, int64_t n, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = x[i], b = y ? y[i] : 0.0;
+  double r;
+  switch (fn) {
+    case 0: r = sd::lit_sin(a); break;
+    case 1: r = sd::lit_cos(a); break;
+    case 2: r = sd::lit_acos(a); break;
+    case 3: r = sd::lit_asin(a); break;
+    case 4: r = sd::lit_atan2(a, b); break;
+    default: r = sd::lit_hypot(a, b); break;
+  }
+  out[i] = r;
+}
+
 __global__ void cubic_roots_kernel(const double* bcd, int64_t n, double* roots,
                                    uint8_t* status) {
   const int64_t i = gtid();
@@ -1594,6 +1710,12 @@ int sd_cubic_roots_f64(const double* bcd, int64_t n, double* roots, uint8_t* sta
 
 int sd_glibc_pow_f64(const double* x, const double* y, int64_t n, double* out, void* stream) {
   SIMPLE_LAUNCH(glibc_pow_kernel, x, y, n, out);
+}
+
+int sd_crlibm_f64(int fn, const double* x, const double* y, int64_t n, double* out,
+                  void* stream) {
+  if (fn < 0 || fn > 5 || (fn >= 4 && !y)) return set_err(SD_EINVAL, "sd_crlibm_f64: bad argument");
+  SIMPLE_LAUNCH(crlibm_kernel, fn, x, y, n, out);
 }
 
 int sd_probe_dfma(int blocks, int iters, double* sink, double* dfma_total, void* stream) {

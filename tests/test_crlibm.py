@@ -99,6 +99,42 @@ def test_exactly_rounded_against_mpmath(cr):
     assert cr.cr_hard_count() == 0
 
 
+def test_quick_phase_equals_accurate_phase(cr):
+    """Two-phase evaluation (sd_crlibm.h): the quick double-double is within
+    2^-76 of the accurate one (the certainty test assumes 2^-70), only
+    ~2^-16 of the calls need the accurate phase, and the two-phase result
+    equals the accurate phase's on every argument."""
+    rng = np.random.default_rng(13)
+    n = 1_000_000
+    j = np.arange(-30, 31) / 32.0
+    x = np.concatenate([j, np.nextafter(j, 5), np.nextafter(j, -5), (np.arange(-60, 61) + 0.5) / 64,
+                        rng.uniform(-7, 7, n), 10 ** rng.uniform(-12, 0, n // 4),
+                        rng.uniform(-1e5, 1e5, n // 8)])
+    cr.cr_quick_sincos_err.restype = ctypes.c_double
+    unc = ctypes.c_long(0)
+    worst = cr.cr_quick_sincos_err(np.ascontiguousarray(x).ctypes.data_as(P), ctypes.c_long(len(x)),
+                                   ctypes.byref(unc))
+    assert worst < 2.0 ** -76, math.log2(worst)
+    assert unc.value < 2e-4 * len(x), unc.value
+
+    def slow(fn, x, y=None):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = x if y is None else np.ascontiguousarray(y, dtype=np.float64)
+        out = np.empty_like(x)
+        cr.cr_eval_slow(fn, x.ctypes.data_as(P), y.ctypes.data_as(P), out.ctypes.data_as(P),
+                        ctypes.c_long(len(x)))
+        return out
+
+    near1 = (1 - 10 ** rng.uniform(-16, -0.3, n // 2)) * rng.choice([-1, 1], n // 2)
+    cases = [(0, x, None), (1, x, None),
+             (2, np.concatenate([rng.uniform(-1, 1, n), near1]), None),
+             (3, np.concatenate([rng.uniform(-1, 1, n), near1, 10 ** rng.uniform(-9, 0, n // 4)]), None),
+             (4, rng.standard_normal(n) * 10 ** rng.uniform(-8, 8, n),
+              rng.standard_normal(n) * 10 ** rng.uniform(-8, 8, n))]
+    for fn, a, b in cases:
+        assert np.array_equal(ev(cr, fn, 0, a, b), slow(fn, a, b), equal_nan=True), fn
+
+
 def test_agrees_with_glibc_where_glibc_rounds_correctly(cr):
     rng = np.random.default_rng(12)
     n = 400_000
