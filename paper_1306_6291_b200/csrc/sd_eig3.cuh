@@ -481,11 +481,21 @@ __device__ __forceinline__ void mm3(const double* a, const double* b, double* c)
 }
 
 // D = rot3x(p1) rot3y(p2) rot3z(p3), evaluated as numpy does ((Rx Ry) Rz)
+// kLit = false: libdevice's sincos instead of the literal solver's
+// correctly rounded one (the polish pass's gate, whose outcome the parity
+// rules check through the residual, not bit for bit)
+template <bool kLit = true>
 __device__ __forceinline__ void compose_rotation(Err& e, const double phi[3], double d[9]) {
   double s1, c1, s2, c2, s3, c3;
-  py_sincos(e, phi[0], &s1, &c1);
-  py_sincos(e, phi[1], &s2, &c2);
-  py_sincos(e, phi[2], &s3, &c3);
+  if (kLit) {
+    py_sincos(e, phi[0], &s1, &c1);
+    py_sincos(e, phi[1], &s2, &c2);
+    py_sincos(e, phi[2], &s3, &c3);
+  } else {
+    sincos(phi[0], &s1, &c1);
+    sincos(phi[1], &s2, &c2);
+    sincos(phi[2], &s3, &c3);
+  }
   const double rx[9] = {1.0, 0.0, 0.0, 0.0, c1, -s1, 0.0, s1, c1};
   const double ry[9] = {c2, 0.0, s2, 0.0, 1.0, 0.0, -s2, 0.0, c2};
   const double rz[9] = {c3, -s3, 0.0, s3, c3, 0.0, 0.0, 0.0, 1.0};

@@ -660,7 +660,8 @@ __device__ __forceinline__ void exact_row(const sd::Sym3& a, T* __restrict__ lam
                                           int64_t i) {
   double l[3], phi[3] = {0.0, 0.0, 0.0}, xs = 1.0;
   int reason = 0;
-  const int cls = sd::classify3_exact(a, l, xs, reason);
+  double sq[2];
+  const int cls = sd::classify3_exact(a, l, xs, reason, sq);
   if (cls == 2) {  // errors and threshold margins: the literal solver
     status[i] = (uint8_t)(sd::kDeferred | (reason << 4));
     return;
@@ -680,8 +681,20 @@ __device__ __forceinline__ void exact_row(const sd::Sym3& a, T* __restrict__ lam
   }
   uint8_t st = 0;
   const double scale = sd::fast_scale(a);
-  const int rc = (cls == 0) ? sd::fast_generic(a, scale, l, phi, st)
-                            : sd::fast_double(a, scale, l, phi, st);
+  int rc;
+  if (cls == 0) {
+    // compute_v / compute_w literally (eig3.py:183-206) on the exact
+    // eigenvalues: the clamps and the V_ZERO_EPS test are the reference's;
+    // an EigenvalueGap / DomainExcursion reroutes in the literal solver
+    double v, w;
+    if (!sd::exact_vw(a, l, sq[0], sq[1], v, w)) {
+      status[i] = (uint8_t)(sd::kDeferred | (6 << 4));
+      return;
+    }
+    rc = sd::generic_rest(a, scale, l, v, w, phi, st);
+  } else {
+    rc = sd::fast_double(a, scale, l, phi, st);
+  }
   if (sizeof(T) != 8 && rc == sd::kFastPolish) {
     status[i] = (uint8_t)(sd::kDeferred | (11 << 4));  // as above
     return;
@@ -755,7 +768,7 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
 #else
     sd::Err e;
     double dm[9];
-    sd::compose_rotation(e, ph, dm);
+    sd::compose_rotation<false>(e, ph, dm);  // libdevice sincos: the gate is residual-checked
     const double rr = sd::abs_residual(dm, lm, a) / sd::fast_scale(a);
     const bool pol = rr > 1e-12 && sd::polish_compact(a, lm, ph);
 #endif

@@ -24,11 +24,10 @@ sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
 OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
-    "base": {"SD_FAST_ONE_ATAN2": 0},
-    "one": {"SD_FAST_ONE_ATAN2": 1},
-    "one_p52": {"SD_FAST_ONE_ATAN2": 1, "SD_VW_PHI_EXP": 52},
-    "one_p48": {"SD_FAST_ONE_ATAN2": 1, "SD_VW_PHI_EXP": 48},
-    "one_p44": {"SD_FAST_ONE_ATAN2": 1, "SD_VW_PHI_EXP": 44},
+    "vw60": {"SD_VW_PHI_EXP": 60},
+    "vw56": {"SD_VW_PHI_EXP": 56},
+    "vw52": {"SD_VW_PHI_EXP": 52},
+    "vw44": {"SD_VW_PHI_EXP": 44},
 }
 
 
