@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -695,10 +696,9 @@ __device__ __forceinline__ void exact_row(const sd::Sym3& a, T* __restrict__ lam
   } else {
     rc = sd::fast_double(a, scale, l, phi, st);
   }
-  if (sizeof(T) != 8 && rc == sd::kFastPolish) {
-    status[i] = (uint8_t)(sd::kDeferred | (11 << 4));  // as above
-    return;
-  }
+  // fp32 rows that need the polish wait like the fast kernel's (store_fast
+  // stashes the fp64 angles in the output bytes); the polish pass recomputes
+  // lambda with classify3_exact, i.e. the values used here
   store_fast<T>(lam, ang, status, i, rc, l, phi, st);
 }
 
@@ -729,12 +729,15 @@ __device__ __forceinline__ void fixup_row(const T* __restrict__ A, T* __restrict
         ph[q] = (double)ang[3 * i + q];
       }
     } else {
-      // fp32: the fast kernel stashed the fp64 angles in the row's output
-      // bytes (store_fast); lambda comes from classify3 again (same code,
-      // same inputs, same value).  TripleRoot rows have zero angles.
+      // fp32: the fast kernel (or the exact pass) stashed the fp64 angles in
+      // the row's output bytes (store_fast); lambda is recomputed — by
+      // classify3 (same code, same inputs, same value as in the fast kernel)
+      // or, where classify3 cannot certify the row (it came through the
+      // exact pass), by classify3_exact.  TripleRoot rows have zero angles.
       double scale = 1.0;
       int reason = 0;
-      const int cls = sd::classify3(a, lm, scale, reason);
+      int cls = sd::classify3(a, lm, scale, reason);
+      if (cls == sd::kClsExact) cls = sd::classify3_exact(a, lm, scale, reason);
       const int pc = st & SD_CODE_MASK;
       const bool ok = pc == sd::kPolishTriple ? cls == 4
                                                : (pc == sd::kPolishDouble ? cls == 3 : cls == 0);
@@ -1545,18 +1548,29 @@ int launch_eig3_fast(const T* A, int64_t n, T* lam, T* ang, uint8_t* status, cud
   const unsigned g2 = (unsigned)fixup_grid(n, SD_FIX_MIN_BLOCKS);
   const unsigned g3 = (unsigned)fixup_grid(n, SD_LIT_MIN_BLOCKS);
   const int vec = aligned(status, 16) ? 1 : 0;
+  // diagnostics (tools/defer_census.py): SD_DEBUG_PASSES=k stops after the
+  // first k of (fast, compaction, exact, polish, literal), leaving the
+  // internal status codes of the rows still pending
+  static const int max_passes = [] {
+    const char* v = getenv("SD_DEBUG_PASSES");
+    return v ? atoi(v) : 5;
+  }();
+  if (max_passes <= 1) return SD_OK;
   if (SD_PASS) {
     launch_after(eig3_pass_kernel<T>, pass_grid(n), kPassThreads, s, A, n, lam, ang, status,
                  vec);
     rc = check_launch("eig3_pass_kernel");
     if (rc != SD_OK) return rc;
   }
+  if (max_passes <= 2) return SD_OK;
   launch_after(eig3_fixup_kernel<T, kFixExact>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
   rc = check_launch("eig3_exact_kernel");
   if (rc != SD_OK) return rc;
+  if (max_passes <= 3) return SD_OK;
   launch_after(eig3_fixup_kernel<T, kFixPolish>, g2, kFixThreads, s, A, n, lam, ang, status, vec);
   rc = check_launch("eig3_polish_kernel");
   if (rc != SD_OK) return rc;
+  if (max_passes <= 4) return SD_OK;
   launch_after(eig3_fixup_kernel<T, kFixLiteral>, g3, kFixThreads, s, A, n, lam, ang, status,
                vec);
   return check_launch("eig3_literal_kernel");
