@@ -288,7 +288,12 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
   constexpr bool kStoreA = kFastRows == 1 && SD_FAST_STORE_A;
   __shared__ __align__(16) T stage[W][32 * 6];
   __shared__ double qa[kStoreA ? 6 : 1][kStoreA ? kFastSlots : 1];
-  __shared__ double ql[3][kFastSlots];
+  // ql[3]: SymMat3.scale from phase A instead of recomputing it in phase B
+  // (SD_FAST_QSCALE: c2 -1.1%, c4 -1.2%, c3 +-0, gpurun r2j)
+#ifndef SD_FAST_QSCALE
+#define SD_FAST_QSCALE 1
+#endif
+  __shared__ double ql[SD_FAST_QSCALE ? 4 : 3][kFastSlots];
   __shared__ int qrow[kFastSlots];
   __shared__ int qgen, qdbl;  // generic rows fill the queue from the front, double roots from the back
 #if SD_FAST_SORT
@@ -361,6 +366,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
       ql[0][slot] = l[0];
       ql[1][slot] = l[1];
       ql[2][slot] = l[2];
+      if (SD_FAST_QSCALE) ql[SD_FAST_QSCALE ? 3 : 0][slot] = scale;
       qrow[slot] = (int)(i - blk0);
     }
   }
@@ -469,7 +475,7 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     double gl[3] = {ql[0][slot], ql[1][slot], ql[2][slot]};
     double phi[3];
     uint8_t st = 0;
-    const double scale = sd::fast_scale(g);
+    const double scale = SD_FAST_QSCALE ? ql[SD_FAST_QSCALE ? 3 : 0][slot] : sd::fast_scale(g);
     const int rc = is_gen ? sd::fast_generic(g, scale, gl, phi, st)
                           : sd::fast_double(g, scale, gl, phi, st);
     store_fast<T>(lam, ang, status, r, rc, gl, phi, st);

@@ -24,10 +24,10 @@ sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
 OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
-    "vw60": {"SD_VW_PHI_EXP": 60},
-    "vw56": {"SD_VW_PHI_EXP": 56},
-    "vw52": {"SD_VW_PHI_EXP": 52},
-    "vw44": {"SD_VW_PHI_EXP": 44},
+    "base": {},
+    "fsq": {"SD_FAST_FNORM_SQ": 1},
+    "fsq_a2": {"SD_FAST_FNORM_SQ": 1, "SD_FAST_ATAN2_OCT": 1, "SD_FAST_ATAN2_OCT_NOFB": 1},
+    "a2": {"SD_FAST_ATAN2_OCT": 1, "SD_FAST_ATAN2_OCT_NOFB": 1},
 }
 
 
