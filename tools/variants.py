@@ -25,9 +25,10 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "base": {},
-    "fsq": {"SD_FAST_FNORM_SQ": 1},
-    "fsq_a2": {"SD_FAST_FNORM_SQ": 1, "SD_FAST_ATAN2_OCT": 1, "SD_FAST_ATAN2_OCT_NOFB": 1},
-    "a2": {"SD_FAST_ATAN2_OCT": 1, "SD_FAST_ATAN2_OCT_NOFB": 1},
+    "onepred": {"SD_FAST_OCT_ONE_PRED": 1},
+    "wrap": {"SD_FAST_WRAP_RANGE": 1},
+    "g1dir": {"SD_FAST_G1_DIR": 1},
+    "all3": {"SD_FAST_OCT_ONE_PRED": 1, "SD_FAST_WRAP_RANGE": 1, "SD_FAST_G1_DIR": 1},
 }
 
 
