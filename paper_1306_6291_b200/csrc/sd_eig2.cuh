@@ -119,8 +119,19 @@ __device__ __forceinline__ double atan_oct(double w) {
   return fma(w * s, p, w);
 }
 
+// SD_EIG2_NULL (diagnostics, tools/eig2_variants.py): 1 = no arithmetic
+// (the kernel's memory time alone), 2 = eigenvalues only (no angle)
+#ifndef SD_EIG2_NULL
+#define SD_EIG2_NULL 0
+#endif
 __device__ __forceinline__ bool diagonalize2_fast(double a11, double a12, double a22, double& l1,
                                                   double& l2, double& phi) {
+#if SD_EIG2_NULL == 1
+  l1 = a11;
+  l2 = a22;
+  phi = a12;
+  return true;
+#endif
   // Branch-free: the range tests only set `ok` (a declined row computes
   // garbage that the caller discards), so several rows' chains interleave.
   const uint32_t h11 = (uint32_t)__double2hiint(a11) & 0x7fffffffu;
@@ -160,6 +171,10 @@ __device__ __forceinline__ bool diagonalize2_fast(double a11, double a12, double
   l1 = 0.5 * (t + r);
   l2 = 0.5 * (t - r);
 
+#if SD_EIG2_NULL == 2
+  phi = q;
+  return ok;
+#endif
   // phi = 0.5 atan2(2 a12 sg, |dd|), sg = sign(dd)
   const double D = P + h;  // in [1, 1 + 2^0.5]
   const double r0 = rcp_approx(D);

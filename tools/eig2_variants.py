@@ -29,11 +29,15 @@ VARIANTS = {
     "literal_r1_t128": {"SD_EIG2_LITERAL": 1, "SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1,
                         "SD_EIG2_THREADS": 128},
     "tile_r2_t128": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128},
-    # round 2: adjacent row pairs read as three 16-byte loads (SD_EIG2_MODE 3)
-    "pair_t128": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 128},
-    "pair_t256": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 256},
-    "pair_t64": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 64},
-    "pair_t128_mb8": {"SD_EIG2_MODE": 3, "SD_EIG2_THREADS": 128, "SD_EIG2_MIN_BLOCKS": 8},
+    # round 2, second half: how the time splits into memory and arithmetic
+    "null_r2_t128": {"SD_EIG2_NULL": 1},
+    "lamonly_r2_t128": {"SD_EIG2_NULL": 2},
+    "null_bulk": {"SD_EIG2_NULL": 1, "SD_EIG2_MODE": 2, "SD_EIG2_THREADS": 256, "SD_EIG2_STAGES": 3,
+                  "SD_EIG2_BLOCKS_PER_SM": 4},
+    "null_stream": {"SD_EIG2_NULL": 1, "SD_EIG2_MODE": 1, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
+                    "SD_EIG2_BLOCKS_PER_SM": 5},
+    "null_r1_t256": {"SD_EIG2_NULL": 1, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 256},
+    "null_r4_t128": {"SD_EIG2_NULL": 1, "SD_EIG2_ROWS": 4},
 }
 
 

@@ -25,10 +25,8 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "base": {},
-    "onepred": {"SD_FAST_OCT_ONE_PRED": 1},
-    "wrap": {"SD_FAST_WRAP_RANGE": 1},
-    "g1dir": {"SD_FAST_G1_DIR": 1},
-    "all3": {"SD_FAST_OCT_ONE_PRED": 1, "SD_FAST_WRAP_RANGE": 1, "SD_FAST_G1_DIR": 1},
+    "gate81": {"SD_GATE_MARGIN2": 0.81},
+    "gate64": {"SD_GATE_MARGIN2": 0.64},
 }
 
 
