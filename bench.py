@@ -768,6 +768,17 @@ def main():
                                       "same flush, interquartile mean of 30 event-timed "
                                       "calls",
                     "kernel_over_copy": kt * 1e3 / fl}
+                # the same kernel on a batch large enough to amortise the
+                # fixed ~8 us of one launch: 2^24 rows of the same generator
+                nb = 1 << 24
+                Ab = make_inputs(c, nb, dev)
+                pb, _, ob = run_hot(sd, Ab, 5, 3, c)
+                kb = statistics.median(pb) * 1e-3
+                extra[c]["same_kernel_2p24_rows"] = {
+                    "n": nb, "value": nb / kb, "unit": "matrices/s", "ms_per_step": kb * 1e3,
+                    "hbm_roofline_frac": cc["bytes"] * nb / kb / 1e9
+                    / result["roofline_hbm"]["peak"], "l2": "inputs > L2"}
+                del Ab, ob
             del Ac, oc
             torch.cuda.empty_cache()
         result["configs_extra"] = extra

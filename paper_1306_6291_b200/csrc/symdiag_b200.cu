@@ -629,8 +629,12 @@ __global__ void __launch_bounds__(kPassThreads, SD_PASS_MIN_BLOCKS)
 
 // Fix-up passes after the fast kernel (and the compaction pass), in order:
 //   kFixExact  : rows marked kExactPending (classify3 could not certify a
-//                decision against glibc's pow) run classify3_exact and the
-//                fast bodies (exact_row);
+//                decision against glibc's pow, or generic_vw found the v / w
+//                decisions or angle magnitudes sensitive to the eigenvalues'
+//                last bits) run classify3_exact — glibc's pow, eigenvalues
+//                with the literal solver's correctly rounded acos / cos —,
+//                compute_v / compute_w literally, and the fast bodies
+//                (exact_row);
 //   kFixPolish : rows marked kPolish* keep their closed-form result and
 //                only run the Gauss-Newton tail (literal residual gate,
 //                then polish_compact);
@@ -653,9 +657,12 @@ constexpr int kFixQueue = kFixTile + kFixThreads;
 #define SD_FIX_POLISH_LITERAL 0
 #endif
 // kExactPending rows (classify3 could not certify a decision against
-// glibc's pow), in their own persistent pass between the compaction pass
-// and the polish pass: classify3_exact (glibc's pow for the powers the
-// gates could not certify), then the fast Generic / DoubleRoot bodies; a
+// glibc's pow; generic_vw could not certify the v / w decisions or angle
+// magnitudes against the reference's eigenvalues), in their own persistent
+// pass between the compaction pass and the polish pass: classify3_exact
+// (glibc's pow for the powers the gates could not certify, acos / cos
+// correctly rounded as in the literal solver), v and w literally on those
+// eigenvalues, then the fast Generic / DoubleRoot bodies; a
 // closed form that needs the Gauss-Newton tail is written with its kPolish*
 // status for the polish pass, errors and threshold margins go to the
 // literal pass.  A pass of its own keeps this rarely run code (and glibc's

@@ -25,8 +25,10 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "base": {},
-    "gate81": {"SD_GATE_MARGIN2": 0.81},
-    "gate64": {"SD_GATE_MARGIN2": 0.64},
+    "mb3": {"SD_FAST_MIN_BLOCKS": 3},
+    "mb5": {"SD_FAST_MIN_BLOCKS": 5},
+    "t128mb8": {"SD_FAST_THREADS": 128, "SD_FAST_MIN_BLOCKS": 8},
+    "t512mb2": {"SD_FAST_THREADS": 512, "SD_FAST_MIN_BLOCKS": 2},
 }
 
 
