@@ -7,7 +7,16 @@ cp $R/bench_sweep.json $P/bench_c2_sweep.json
 cp $R/bench_reference.json $P/bench_reference.json
 cp $R/launches_c2.csv $R/launches_c3.csv $R/launches_c4.csv $P/
 cp $R/pytest_gpu.log $R/smoke.log $R/env.txt $P/
-cp $R/ncu_summary.json profiles/ncu_summary.json
+python - <<PY
+import json
+new = json.load(open('$R/ncu_summary.json'))
+try:
+    old = json.load(open('profiles/ncu_summary.json'))
+except (OSError, ValueError):
+    old = {}
+old.update(new)  # keeps the other configs' captures (c3: profiles/r2/ncu_summary_c3.json)
+json.dump(old, open('profiles/ncu_summary.json', 'w'), indent=1)
+PY
 rm -rf $P/parity $P/parity_sweep
 cp -r $R/parity $P/parity
 mkdir -p $P/parity_sweep
