@@ -278,12 +278,19 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
     eig3_fast_kernel(const T* __restrict__ A, int64_t n, T* __restrict__ lam,
                      T* __restrict__ ang, uint8_t* __restrict__ status) {
   constexpr int W = kFastThreads / 32;
-  // Phase B re-reads its row of A from global memory (an L2 hit: the block
-  // staged it moments ago) rather than parking it in shared memory: 12 KB
-  // less shared memory per block leaves more L1 for the spill traffic and
-  // measured 1-3% faster (profiles/r1_variants12_rows_storeA.jsonl).
+  // Phase B does not park A in a queue-ordered shared array of its own
+  // (SD_FAST_STORE_A: 12 KB more shared memory per block measured 1-3%
+  // slower, profiles/r1_variants12_rows_storeA.jsonl); it re-reads the row
+  // from the staging tile of phase A (SD_FAST_STAGE_REUSE below), or from
+  // global memory (an L2 hit) when several tiles share the buffer.
 #ifndef SD_FAST_STORE_A
 #define SD_FAST_STORE_A 0
+#endif
+  // SD_FAST_STAGE_REUSE: phase B reads its row from the staging tile of
+  // phase A (still intact: one tile per warp and block) instead of global
+  // memory: c2 -0.4%, c3 -1.0%, c4 -0.5% (gpurun r3a)
+#ifndef SD_FAST_STAGE_REUSE
+#define SD_FAST_STAGE_REUSE 1
 #endif
   constexpr bool kStoreA = kFastRows == 1 && SD_FAST_STORE_A;
   __shared__ __align__(16) T stage[W][32 * 6];
@@ -469,6 +476,10 @@ __global__ void __launch_bounds__(kFastThreads, SD_FAST_MIN_BLOCKS)
       g.a22 = qa[3][slot];
       g.a23 = qa[4][slot];
       g.a33 = qa[5][slot];
+    } else if (SD_FAST_STAGE_REUSE && kFastRows == 1) {
+      // the row is still in the shared-memory tile its warp staged in phase A
+      const int q = qrow[slot];
+      g = load_row(&stage[q >> 5][6 * (q & 31)]);
     } else {
       g = load_row(A + 6 * r);
     }

@@ -25,10 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "base": {},
-    "mb3": {"SD_FAST_MIN_BLOCKS": 3},
-    "mb5": {"SD_FAST_MIN_BLOCKS": 5},
-    "t128mb8": {"SD_FAST_THREADS": 128, "SD_FAST_MIN_BLOCKS": 8},
-    "t512mb2": {"SD_FAST_THREADS": 512, "SD_FAST_MIN_BLOCKS": 2},
+    "stage": {"SD_FAST_STAGE_REUSE": 1},
 }
 
 
