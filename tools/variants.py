@@ -25,7 +25,7 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "base": {},
-    "stage": {"SD_FAST_STAGE_REUSE": 1},
+    "intcmp": {"SD_FAST_INT_CMP": 1},
 }
 
 
