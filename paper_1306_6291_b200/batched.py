@@ -483,6 +483,59 @@ def _scalar_plan():
     return plan
 
 
+class _ScalarScratch(__import__("threading").local):
+    """Per-thread staging for the n = 1 drop-in calls: one float64 buffer
+    (inputs and every output of one row) and one status byte, allocated once
+    with their addresses cached — the scalar calls then cost one C call plus
+    a tolist(), not five numpy allocations and ctypes pointer objects."""
+
+    def __init__(self):
+        import numpy as np
+        self.buf = np.zeros(64)          # A[0:6] lam[6:9] ang[9:12] rep[12:36] d[36:45]
+        self.st = np.zeros(8, np.uint8)
+        self.p = self.buf.ctypes.data
+        self.ps = self.st.ctypes.data
+        self.fn3 = self.fn2 = None
+
+
+_scratch = _ScalarScratch()
+
+
+def eig3_report_scalar(packed):
+    """One 3x3 matrix (a11, a12, a13, a22, a23, a33) through
+    sd_eig3_report_f64_host -> (status, lam[3], ang[3], rep[24], d[9]) as
+    Python scalars / lists."""
+    sc = _scratch
+    if sc.fn3 is None:
+        sc.fn3 = _lib.load().sd_eig3_report_f64_host
+    sc.buf[0:6] = packed
+    p = sc.p
+    with _scalar_lock:
+        plan = _scalar_plan()
+        rc = sc.fn3(plan._h, p, 1, p + 48, p + 72, sc.ps, p + 96, p + 288)
+    if rc != _lib.SD_OK:
+        _lib.call("sd_eig3_report_f64_host", plan._h, p, 1, p + 48, p + 72, sc.ps, p + 96, p + 288)
+    v = sc.buf[6:45].tolist()
+    return int(sc.st[0]), v[0:3], v[3:6], v[6:30], v[30:39]
+
+
+def eig2_report_scalar(packed):
+    """One 2x2 matrix (a11, a12, a22) through sd_eig2_report_f64_host ->
+    (status, lam[2], phi, d[4]) as Python scalars / lists."""
+    sc = _scratch
+    if sc.fn2 is None:
+        sc.fn2 = _lib.load().sd_eig2_report_f64_host
+    sc.buf[0:3] = packed
+    p = sc.p
+    with _scalar_lock:
+        plan = _scalar_plan()
+        rc = sc.fn2(plan._h, p, 1, p + 48, p + 72, sc.ps, p + 288)
+    if rc != _lib.SD_OK:
+        _lib.call("sd_eig2_report_f64_host", plan._h, p, 1, p + 48, p + 72, sc.ps, p + 288)
+    v = sc.buf[6:40].tolist()
+    return int(sc.st[0]), v[0:2], v[3], v[30:34]
+
+
 def eig3_report_host(A, report: bool = True, with_d: bool = True):
     """sd_eig3_report_f64_host on host rows A[n,6] -> numpy (lam, ang,
     status, report | None, d | None); one synchronous C call."""

@@ -128,9 +128,17 @@ int ensure_report_buffers(sd_plan* p) {
 int ensure_small(sd_plan* p) {
   if (p->small_dev && p->small_host) return SD_OK;
   cudaError_t e = cudaMalloc((void**)&p->small_dev, kSmallBytes);
-  if (e == cudaSuccess) e = cudaHostAlloc((void**)&p->small_host, kSmallBytes, cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&p->small_host, kSmallBytes, cudaHostAllocMapped);
   return e == cudaSuccess ? SD_OK : herr(SD_ECUDA, "sd_*_report_host: allocation", e);
 }
+
+// Scalar-sized calls run zero-copy: the kernel reads A from, and writes
+// every output to, the pinned mirror through its device mapping (a few
+// hundred bytes over PCIe), so the call is one launch and one wait instead
+// of H2D + launch + D2H (SD_SMALL_ZERO_COPY=0: the staged copies).
+#ifndef SD_SMALL_ZERO_COPY
+#define SD_SMALL_ZERO_COPY 1
+#endif
 
 // n <= kSmallRows: stage A in the pinned mirror, one H2D, `launch` on the
 // packed device region, one D2H of every output, wait, unpack.
@@ -145,7 +153,21 @@ int run_small(sd_plan* plan, int64_t m, int win, const double* A, Launch launch,
   double* h = reinterpret_cast<double*>(plan->small_host);
   double* dv = reinterpret_cast<double*>(plan->small_dev);
   std::memcpy(h, A, (size_t)m * win * sizeof(double));
-  cudaError_t e = cudaMemcpyAsync(dv, h, (size_t)m * win * sizeof(double), cudaMemcpyHostToDevice, s);
+  cudaError_t e;
+#if SD_SMALL_ZERO_COPY
+  double* hm = nullptr;  // device address of the mapped mirror
+  if (cudaHostGetDevicePointer((void**)&hm, h, 0) == cudaSuccess && hm) {
+    rc = launch(hm, hm + 6 * m, hm + 9 * m, hm + 12 * m, hm + 36 * m,
+                reinterpret_cast<uint8_t*>(hm + 45 * m), s);
+    if (rc != SD_OK) return rc;
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return herr(SD_ECUDA, "sd_*_report_host", e);
+    unpack(h + 6 * m, h + 9 * m, h + 12 * m, h + 36 * m, reinterpret_cast<uint8_t*>(h + 45 * m));
+    return SD_OK;
+  }
+  (void)cudaGetLastError();
+#endif
+  e = cudaMemcpyAsync(dv, h, (size_t)m * win * sizeof(double), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return herr(SD_ECUDA, "H2D copy", e);
   rc = launch(dv, dv + 6 * m, dv + 9 * m, dv + 12 * m, dv + 36 * m,
               reinterpret_cast<uint8_t*>(dv + 45 * m), s);

@@ -172,15 +172,14 @@ def degenerate_double(a: SymMat3, lam, lam3):
 
 def diagonalize3(a: SymMat3) -> EigenDecomp3:
     """diagonalize3 (eig3.py:509-565) through the fused B200 kernel."""
-    lam, ang, st, rep, d = batched.eig3_report_host([a.packed()])  # one synchronous C call
-    st = int(st[0])
+    st, lam, ang, rep, d = batched.eig3_report_scalar(a.packed())  # one synchronous C call
     c = st & S.CODE_MASK
     if c >= S.ERR_FIRST:
         S.raise_for(c, "diagonalize3")
-    l1, l2, l3 = lam[0].tolist()
-    return EigenDecomp3(lambda1=l1, lambda2=l2, lambda3=l3, angles=Angles3(*ang[0].tolist()),
-                        d=d[0].reshape(3, 3), branch=_BRANCH[c],
-                        report=_report_from_row(st, rep[0]))
+    l1, l2, l3 = lam
+    return EigenDecomp3(lambda1=l1, lambda2=l2, lambda3=l3, angles=Angles3(*ang),
+                        d=np.array(d).reshape(3, 3), branch=_BRANCH[c],
+                        report=_report_from_row(st, rep))
 
 
 def euler_angles(dec: EigenDecomp3) -> Angles3:
