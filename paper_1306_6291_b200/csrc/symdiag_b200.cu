@@ -658,8 +658,12 @@ __global__ void __launch_bounds__(kPassThreads, SD_PASS_MIN_BLOCKS)
 // one-row blocks, no global workspace.  Separate launches keep each
 // kernel's code small (the literal solver is ~13k SASS instructions).
 constexpr int kFixTile = 4096;  // 32 status bytes per thread
+// exact and polish passes: 6 resident blocks of 128 threads (<= 85
+// registers); 3 / 4 / 6 measured on 2^24 rows (gpurun r3f): c3 1.894 /
+// 1.858 / 1.855 ms (exact pass 104 / 91 / 81 us), c4 1.754 / 1.736 / 1.727.
+// The literal pass keeps 4 (SD_LIT_MIN_BLOCKS, 128 registers).
 #ifndef SD_FIX_MIN_BLOCKS
-#define SD_FIX_MIN_BLOCKS 4
+#define SD_FIX_MIN_BLOCKS 6
 #endif
 constexpr int kFixThreads = 128;
 constexpr int kFixQueue = kFixTile + kFixThreads;
@@ -839,7 +843,7 @@ __device__ __forceinline__ unsigned fix_mine4(unsigned w) {
 // few rows: SD_LIT_MIN_BLOCKS resident blocks (register cap vs spills; 2, 3,
 // 6, 8 measured no better than 4, profiles/r1_variants28_literal_blocks.jsonl).
 #ifndef SD_LIT_MIN_BLOCKS
-#define SD_LIT_MIN_BLOCKS SD_FIX_MIN_BLOCKS
+#define SD_LIT_MIN_BLOCKS 4
 #endif
 template <typename T, int kMode>
 __global__ void __launch_bounds__(kFixThreads, kMode != kFixLiteral ? SD_FIX_MIN_BLOCKS : SD_LIT_MIN_BLOCKS)

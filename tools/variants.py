@@ -25,7 +25,10 @@ OUT = ROOT / "paper_1306_6291_b200" / "lib" / "variants"
 
 VARIANTS = {
     "base": {},
-    "intcmp": {"SD_FAST_INT_CMP": 1},
+    "pass4": {"SD_PASS_MIN_BLOCKS": 4},
+    "pass2": {"SD_PASS_MIN_BLOCKS": 2},
+    "fix6": {"SD_FIX_MIN_BLOCKS": 6, "SD_LIT_MIN_BLOCKS": 4},
+    "fix3": {"SD_FIX_MIN_BLOCKS": 3, "SD_LIT_MIN_BLOCKS": 4},
 }
 
 
