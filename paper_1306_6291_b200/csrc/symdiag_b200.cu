@@ -979,7 +979,13 @@ unsigned pass_grid(int64_t n) {
 #define SD_EIG2_BLOCKS_PER_SM 4
 #endif
 #ifndef SD_EIG2_MIN_BLOCKS
-#define SD_EIG2_MIN_BLOCKS 1  // __launch_bounds__ minimum resident blocks (register cap)
+// __launch_bounds__ minimum resident blocks (register cap).  12 blocks of
+// 128 threads = 48 warps / SM at <= 40 registers: the one-launch c1 batch
+// (2^20 rows, latency-bound) does not care (14.3 us at 1 / 8 / 10 / 12), a
+// throughput-sized batch does: 2^24 rows 112 G/s uncapped (80 registers, 24
+// warps), 123 at 8, 128.5 at 10, 129.7 at 12 (0.98 of the HBM roofline), 95
+// at 14 (spills); gpurun r3j / r3k.
+#define SD_EIG2_MIN_BLOCKS 12
 #endif
 constexpr int kEig2Rows = SD_EIG2_ROWS;
 constexpr int kEig2Threads = SD_EIG2_THREADS;

@@ -29,15 +29,11 @@ VARIANTS = {
     "literal_r1_t128": {"SD_EIG2_LITERAL": 1, "SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 1,
                         "SD_EIG2_THREADS": 128},
     "tile_r2_t128": {"SD_EIG2_MODE": 0, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128},
-    # round 2, second half: how the time splits into memory and arithmetic
-    "null_r2_t128": {"SD_EIG2_NULL": 1},
-    "lamonly_r2_t128": {"SD_EIG2_NULL": 2},
-    "null_bulk": {"SD_EIG2_NULL": 1, "SD_EIG2_MODE": 2, "SD_EIG2_THREADS": 256, "SD_EIG2_STAGES": 3,
-                  "SD_EIG2_BLOCKS_PER_SM": 4},
-    "null_stream": {"SD_EIG2_NULL": 1, "SD_EIG2_MODE": 1, "SD_EIG2_ROWS": 2, "SD_EIG2_THREADS": 128,
-                    "SD_EIG2_BLOCKS_PER_SM": 5},
-    "null_r1_t256": {"SD_EIG2_NULL": 1, "SD_EIG2_ROWS": 1, "SD_EIG2_THREADS": 256},
-    "null_r4_t128": {"SD_EIG2_NULL": 1, "SD_EIG2_ROWS": 4},
+    "tile_r2_t128_mb10": {"SD_EIG2_MIN_BLOCKS": 10},
+    "tile_r2_t128_mb12": {"SD_EIG2_MIN_BLOCKS": 12},
+    "tile_r2_t128_mb14": {"SD_EIG2_MIN_BLOCKS": 14},
+    "tile_r1_t128_mb12": {"SD_EIG2_ROWS": 1, "SD_EIG2_MIN_BLOCKS": 12},
+    "tile_r1_t128_mb16": {"SD_EIG2_ROWS": 1, "SD_EIG2_MIN_BLOCKS": 16},
 }
 
 
